@@ -1,0 +1,192 @@
+/*
+ * qtree_cuda.h -- C ABI of the B200 quantization-tree transition estimator
+ * (libqtree_cuda.so, built from paper_1101_3228_b200/csrc/ for sm_100a).
+ *
+ * This is the drop-in boundary for the reference's hot path (arXiv 1101.3228,
+ * reference tree /root/reference/proj/include/qtree, cited below as
+ * <file>:<line>). Every entry point is plain C: pointers, sizes and integer
+ * status codes, no C++ or torch types. The C++ headers under include/qtree/
+ * re-expose the reference's own API (qtree::tree::estimate_alg1 ...) on top of
+ * these calls; INTEGRATION.md shows how a reference user switches over.
+ *
+ * Array layouts (identical to the reference's CountMatrixSet / QuantTree
+ * flattened in layer order, quant_tree.hpp:20-84):
+ *   sizes[0..n]   layer sizes, sizes[0] == 1 (layer 0 is the start point x0)
+ *   points        layers 1..n concatenated, row-major N_k x dim doubles
+ *   visits        layers 0..n concatenated, sum_k N_k  u64
+ *   joint, pi     transitions 1..n concatenated, row-major N_{k-1} x N_k
+ *
+ * Threading: every call is synchronous unless it takes a stream; calls on
+ * distinct plans are reentrant. There is no CPU fallback: without a usable
+ * sm_100 device every compute entry returns QT_ERR_DEVICE.
+ */
+#ifndef QTREE_CUDA_H
+#define QTREE_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QT_API __attribute__((visibility("default")))
+
+/* Status codes. The C++ shim maps them back to the reference's exceptions:
+ * 1 -> std::invalid_argument, 2 -> qtree::ConfigError, 3 -> qtree::IoError,
+ * 4 -> qtree::NumericError (errors.hpp:9-21), 5 -> NumericError("cuda: ...")
+ * so the CLI exit-code contract 1/2/3 (qtree_main.cpp:291-303) is kept. */
+typedef enum {
+  QT_OK = 0,
+  QT_ERR_INVALID_ARGUMENT = 1,
+  QT_ERR_CONFIG = 2,
+  QT_ERR_IO = 3,
+  QT_ERR_NUMERIC = 4,
+  QT_ERR_DEVICE = 5
+} qt_status;
+
+/* rng::EngineKind order (stream.hpp:16) */
+typedef enum { QT_ENGINE_LCG48 = 0, QT_ENGINE_MRG32K3A = 1, QT_ENGINE_XORWOW = 2 } qt_engine;
+
+/* tree::EstimatorKind order (estimate.hpp:18) */
+typedef enum { QT_ALG_I = 0, QT_ALG_II = 1, QT_ALG_III = 2 } qt_estimator;
+
+/* The closed set of chains the device path implements (model/chains.hpp:17-26
+ * is a template concept; the drop-in headers static_assert on this set). */
+typedef enum {
+  QT_CHAIN_BROWNIAN_1D = 0, /* BrownianChain1d, chains.hpp:68-95 */
+  QT_CHAIN_TWO_FACTOR = 1,  /* TwoFactorChain, chains.hpp:30-64 */
+  QT_CHAIN_OU_1D = 2,       /* new (config 3): factor 1 of TwoFactorChain */
+  QT_CHAIN_GBM_3D = 3       /* new (config 5): 3-D correlated Brownian log-state */
+} qt_chain_kind;
+
+/* Chain coefficients, computed on the HOST with the reference formulas so the
+ * FP64 constants are bit-identical (two_factor.hpp:57-101, chains.hpp:78-90).
+ * step:     n rows of 6 doubles, row t = transition t -> t+1
+ *   BROWNIAN_1D: [sqrt(dt)]             TWO_FACTOR: [a1, a2, l11, l21, l22]
+ *   OU_1D:       [a, -, s]              GBM_3D:     [c00, c10, c11, c20, c21, c22]
+ * marginal: n+1 rows of 6 doubles, row k = factor of the law of X_k (Alg III)
+ *   BROWNIAN_1D: [sqrt(k dt)] (k = 0 gives exactly 0.0, chains.hpp:89)
+ *   TWO_FACTOR:  [l11, l21, l22]   OU_1D: [sd]   GBM_3D: lower triangle as step */
+typedef struct {
+  int32_t kind;  /* qt_chain_kind */
+  int32_t layers;
+  const double* step;
+  const double* marginal;
+} qt_chain;
+
+/* Model parameters (qtree::model::TwoFactorParams, two_factor.hpp:16-26, plus
+ * the GBM basket correlations of the config-5 chain). */
+typedef struct {
+  double s0, sigma1, sigma2, alpha1, alpha2, rho, r, strike, horizon;
+  int32_t steps;
+  double gbm_rho[3]; /* rho12, rho13, rho23 */
+} qt_model_params;
+
+/* Host-side coefficients of a chain with the reference formulas
+ * (Ar1Spec::from_params two_factor.hpp:90-101, ou_covariance/cholesky2 :57-77,
+ * BrownianChain1d chains.hpp:68-95). Errors as the reference constructors:
+ * ConfigError for invalid parameters, NumericError for degenerate ones. */
+QT_API qt_status qt_chain_coefficients(int32_t kind, const qt_model_params* params, double* step,
+                                       double* marginal);
+
+typedef struct {
+  int32_t dim;
+  int32_t layers;
+  const uint64_t* sizes;  /* n+1 entries, sizes[0] == 1 */
+  const double* points;   /* layers 1..n */
+} qt_grids;
+
+/* ---- one-call estimator (host buffers in and out) ------------------------ */
+
+/* tree::estimate(kind, chain, grids, samples, opt) (estimate.hpp:299-309):
+ * Alg I / II: `samples` paths, path m on the m-th block substream of
+ * 2*ceil(n*nps/2) uniforms (estimate.hpp:48-50,97-98); Alg III: `samples` per
+ * layer, sample (k,m) on substream (k-1)*samples+m (estimate.hpp:228-248).
+ * `devices` > 1 shards the units over that many GPUs of this process and sums
+ * the partial counts with one NCCL all-reduce; counts are bit-identical for
+ * any device count. phases_ms (nullable) receives the BuildPhases fields
+ * {simulate, nn, merge, normalize, total} (estimate.hpp:22-28). */
+QT_API qt_status qt_estimate(int32_t estimator, const qt_chain* chain, const qt_grids* grids,
+                             uint64_t samples, int32_t engine, uint64_t seed, int32_t devices,
+                             uint64_t* visits, uint64_t* joint, double* pi, double* phases_ms);
+
+/* Parity mode: the caller supplies every normal (path-major, n*nps per path
+ * for Alg I/II; d+nps per sample, layer-major, for Alg III) instead of the
+ * in-kernel stream. Counts are then bit-exact by construction. */
+QT_API qt_status qt_estimate_normals(int32_t estimator, const qt_chain* chain,
+                                     const qt_grids* grids, uint64_t samples,
+                                     const double* normals, uint64_t* visits, uint64_t* joint,
+                                     double* pi);
+
+/* detail::accumulate_paths over the window [first, first+count) of a run of
+ * `total` paths (estimate.hpp:88-126). ADDS into visits/joint. */
+QT_API qt_status qt_accumulate_paths(const qt_chain* chain, const qt_grids* grids,
+                                     int32_t engine, uint64_t seed, uint64_t first,
+                                     uint64_t count, uint64_t total, uint64_t* visits,
+                                     uint64_t* joint);
+
+/* ---- device-resident plan (grids staged once; used by the bench and by
+ *      multi-process sharding under torch.distributed) ---------------------- */
+
+typedef struct qt_plan qt_plan;
+
+QT_API qt_status qt_plan_create(const qt_chain* chain, const qt_grids* grids, int32_t device,
+                                qt_plan** out);
+QT_API qt_status qt_plan_destroy(qt_plan* plan);
+QT_API qt_status qt_plan_layout(const qt_plan* plan, uint64_t* n_visits, uint64_t* n_joint);
+
+/* Count units [first, first+count) of `total` into d_joint (device u64,
+ * n_joint entries, ADDED to). Alg I/II: units are paths; Alg III: units are
+ * the layer-major sample indices (k-1)*M + m, total = n*M. d_normals is NULL
+ * for the in-kernel engine, else a device array of the window's normals.
+ * Asynchronous on `stream` (a cudaStream_t; NULL = default stream).
+ * *launches (nullable) receives the number of kernels enqueued. */
+QT_API qt_status qt_plan_count(qt_plan* plan, int32_t estimator, int32_t engine, uint64_t seed,
+                               uint64_t first, uint64_t count, uint64_t total,
+                               const double* d_normals, uint64_t* d_joint, void* stream,
+                               int32_t* launches);
+
+/* Derives visits from the summed joint counts and row-normalises pi
+ * (quant_tree.hpp:69-83; estimate.hpp:118-119,261,275-281). `samples` is M
+ * (paths, or samples per layer for Alg III). Device pointers, async. */
+QT_API qt_status qt_plan_finalize(qt_plan* plan, int32_t estimator, uint64_t samples,
+                                  const uint64_t* d_joint, uint64_t* d_visits, double* d_pi,
+                                  void* stream, int32_t* launches);
+
+/* ---- Voronoi projection (nn.hpp:18-46), batch form of NnIndex::nearest ---- */
+QT_API qt_status qt_nearest(int32_t dim, uint64_t n_points, const double* points,
+                            uint64_t n_queries, const double* queries, uint64_t* out);
+
+/* ---- backward dynamic programming (pricer/bdp.hpp, pricer/swing.hpp) ------
+ * phi: the NodePayoff tabulated per node, laid out like visits. */
+QT_API qt_status qt_bdp_stopping(int32_t layers, const uint64_t* sizes, const uint64_t* visits,
+                                 const double* pi, const double* phi, double* value,
+                                 uint8_t* exercise, double* price);
+/* value_all (nullable): per layer k, (m - m_lo[k]) * N_k + i (swing.hpp:23-39) */
+QT_API qt_status qt_bdp_swing(int32_t layers, const uint64_t* sizes, const uint64_t* visits,
+                              const double* pi, const double* phi, int32_t q_min, int32_t q_max,
+                              double* price, double* value_all);
+
+/* ---- diagnostics ----------------------------------------------------------- */
+
+/* The exact normals the in-kernel engine feeds path m in [first, first+count)
+ * (PathStreamer + Box-Muller, stream.hpp:57-62,97-108,182-231). */
+QT_API qt_status qt_path_normals(int32_t engine, uint64_t seed, uint64_t normals_per_path,
+                                 uint64_t first, uint64_t count, double* out);
+/* Raw uniforms of the serial stream from draw `offset` (MRG32k3a/LCG48). */
+QT_API qt_status qt_uniforms(int32_t engine, uint64_t seed, uint64_t offset, uint64_t count,
+                             double* out);
+
+/* Thread-local text of the last failure on this thread. */
+QT_API const char* qt_last_error(void);
+/* Build identification: "qtree_cuda <version> sm_100a ..." */
+QT_API const char* qt_version(void);
+/* Number of kernels this library has launched in this process (evidence
+ * counter for the bench's gpu_launches). */
+QT_API uint64_t qt_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QTREE_CUDA_H */

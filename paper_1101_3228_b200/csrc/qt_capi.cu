@@ -1,0 +1,953 @@
+// qt_capi.cu -- host runtime behind include/qtree_cuda.h.
+//
+// Owns: validation with the reference's error taxonomy, the per-layer grid
+// tables (sorted 1-D records + bucket index, or raw points for d >= 2), the
+// RNG jump tables, device plans, multi-GPU sharding with one NCCL all-reduce,
+// and the one-call host-buffer entry points. No CPU compute fallback exists:
+// every count is produced by the kernels in qt_kernels.cu.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <memory>
+#include <vector>
+
+#include "../../include/qtree_cuda.h"
+#include "qt_internal.h"
+#include "qt_layout.h"
+
+namespace {
+
+using qt::LayerTable;
+using qt::Rec1;
+
+thread_local std::string g_error;
+std::atomic<uint64_t> g_launches{0};
+
+struct Failure {
+  qt_status code;
+  std::string msg;
+};
+
+[[noreturn]] void raise(qt_status c, const std::string& m) { throw Failure{c, m}; }
+
+#define QT_CUDA(expr)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      raise(QT_ERR_DEVICE, std::string("cuda: ") + cudaGetErrorString(e_) + " (" #expr ")"); \
+  } while (0)
+
+template <class F>
+qt_status guarded(F&& f) {
+  try {
+    f();
+    return QT_OK;
+  } catch (const Failure& e) {
+    g_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_error = "host allocation failed";
+    return QT_ERR_DEVICE;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return QT_ERR_DEVICE;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// RNG jump tables (host side of mrg32k3a_skip / lcg48_skip)
+// ---------------------------------------------------------------------------
+using u128 = unsigned __int128;
+constexpr uint64_t kM1 = 4294967087ull, kM2 = 4294944443ull;
+
+struct Mat3 {
+  uint64_t a[3][3];
+};
+
+Mat3 mat_mul(const Mat3& x, const Mat3& y, uint64_t m) {
+  Mat3 r{};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      u128 acc = 0;
+      for (int k = 0; k < 3; ++k) acc += static_cast<u128>(x.a[i][k]) * y.a[k][j];
+      r.a[i][j] = static_cast<uint64_t>(acc % m);
+    }
+  return r;
+}
+
+// J^(2^b), b = 0..63, both components: [b][0..8] = m1 part, [b][9..17] = m2 part
+std::vector<uint32_t> mrg_jump_table() {
+  Mat3 c1{{{0, 1, 0}, {0, 0, 1}, {kM1 - 810728ull, 1403580ull, 0}}};
+  Mat3 c2{{{0, 1, 0}, {0, 0, 1}, {kM2 - 1370589ull, 0, 527612ull}}};
+  std::vector<uint32_t> t(64 * 18);
+  for (int b = 0; b < 64; ++b) {
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        t[b * 18 + 3 * i + j] = static_cast<uint32_t>(c1.a[i][j]);
+        t[b * 18 + 9 + 3 * i + j] = static_cast<uint32_t>(c2.a[i][j]);
+      }
+    c1 = mat_mul(c1, c1, kM1);
+    c2 = mat_mul(c2, c2, kM2);
+  }
+  return t;
+}
+
+constexpr uint64_t kLcgMask = (1ull << 48) - 1;
+std::vector<unsigned long long> lcg_jump_table() {
+  std::vector<unsigned long long> t(128);
+  uint64_t A = 0x5DEECE66Dull, C = 0xBull;
+  for (int b = 0; b < 64; ++b) {
+    t[2 * b] = A;
+    t[2 * b + 1] = C;
+    const uint64_t A2 = (A * A) & kLcgMask, C2 = (A * C + C) & kLcgMask;
+    A = A2;
+    C = C2;
+  }
+  return t;
+}
+
+uint64_t splitmix64(uint64_t& z) {
+  z += 0x9E3779B97F4A7C15ull;
+  uint64_t v = z;
+  v = (v ^ (v >> 30)) * 0xBF58476D1CE4E5B9ull;
+  v = (v ^ (v >> 27)) * 0x94D049BB133111EBull;
+  return v ^ (v >> 31);
+}
+
+// Device-resident copies of the jump tables, one per device.
+struct DeviceTables {
+  uint32_t* mrg = nullptr;
+  unsigned long long* lcg = nullptr;
+};
+std::mutex g_dev_mu;
+DeviceTables g_dev_tables[64];
+
+const DeviceTables& device_tables(int dev) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  DeviceTables& t = g_dev_tables[dev];
+  if (!t.mrg) {
+    const auto m = mrg_jump_table();
+    const auto l = lcg_jump_table();
+    QT_CUDA(cudaMalloc(&t.mrg, m.size() * sizeof(uint32_t)));
+    QT_CUDA(cudaMalloc(&t.lcg, l.size() * sizeof(unsigned long long)));
+    QT_CUDA(cudaMemcpy(t.mrg, m.data(), m.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    QT_CUDA(cudaMemcpy(t.lcg, l.data(), l.size() * sizeof(unsigned long long),
+                       cudaMemcpyHostToDevice));
+  }
+  return t;
+}
+
+qt::SrcArgs make_src(int dev, int engine, uint64_t seed, uint64_t draws, uint32_t per_unit,
+                     const double* normals, uint64_t normals_first) {
+  qt::SrcArgs a{};
+  // mrg32k3a_seed (mrg32k3a.hpp:34-40)
+  uint64_t z = seed;
+  for (int i = 0; i < 3; ++i) a.mrg_seed[i] = static_cast<uint32_t>(1 + splitmix64(z) % (kM1 - 1));
+  for (int i = 0; i < 3; ++i)
+    a.mrg_seed[3 + i] = static_cast<uint32_t>(1 + splitmix64(z) % (kM2 - 1));
+  a.lcg_seed = ((seed << 16) | 0x330Eull) & kLcgMask;  // lcg48_seed (lcg48.hpp:20-22)
+  a.seed = seed;
+  const DeviceTables& t = device_tables(dev);
+  a.mrg_table = t.mrg;
+  a.lcg_table = t.lcg;
+  a.normals = normals;
+  a.normals_first = normals_first;
+  a.draws = draws;
+  a.per_unit = per_unit;
+  (void)engine;
+  return a;
+}
+
+// ---------------------------------------------------------------------------
+// chains
+// ---------------------------------------------------------------------------
+int chain_dim(int kind) {
+  switch (kind) {
+    case QT_CHAIN_BROWNIAN_1D: return 1;
+    case QT_CHAIN_TWO_FACTOR: return 2;
+    case QT_CHAIN_OU_1D: return 1;
+    case QT_CHAIN_GBM_3D: return 3;
+  }
+  raise(QT_ERR_INVALID_ARGUMENT, "estimate: unknown chain kind");
+}
+
+// ou_covariance (two_factor.hpp:57-63)
+void ou_cov(double t, double a1, double a2, double rho, double c[3]) {
+  c[0] = -std::expm1(-2.0 * a1 * t) / (2.0 * a1);
+  c[2] = -std::expm1(-2.0 * a2 * t) / (2.0 * a2);
+  c[1] = -rho * std::expm1(-(a1 + a2) * t) / (a1 + a2);
+}
+
+// cholesky2 (two_factor.hpp:67-77)
+void chol2(const double c[3], double l[3]) {
+  if (c[0] < 0.0 || c[2] < 0.0) raise(QT_ERR_NUMERIC, "cholesky2: negative variance");
+  l[0] = std::sqrt(c[0]);
+  l[1] = l[0] > 0.0 ? c[1] / l[0] : 0.0;
+  const double rem = c[2] - l[1] * l[1];
+  if (rem < -1e-12 * std::max(1.0, c[2]))
+    raise(QT_ERR_NUMERIC, "cholesky2: covariance not positive semi-definite");
+  l[2] = std::sqrt(std::max(0.0, rem));
+}
+
+void validate_params(const qt_model_params& p) {
+  auto fail = [](const char* key, const char* what) {
+    raise(QT_ERR_CONFIG, std::string("parameter '") + key + "' " + what);
+  };
+  if (!(p.s0 > 0.0)) fail("s0", "must be > 0");
+  if (!(p.sigma1 >= 0.0)) fail("sigma1", "must be >= 0");
+  if (!(p.sigma2 >= 0.0)) fail("sigma2", "must be >= 0");
+  if (!(p.alpha1 > 0.0)) fail("alpha1", "must be > 0");
+  if (!(p.alpha2 > 0.0)) fail("alpha2", "must be > 0");
+  if (!(p.rho >= -1.0 && p.rho <= 1.0)) fail("rho", "must lie in [-1, 1]");
+  if (!std::isfinite(p.r)) fail("r", "must be finite");
+  if (!(p.strike > 0.0)) fail("K", "must be > 0");
+  if (!(p.horizon > 0.0)) fail("T", "must be > 0");
+  if (p.steps < 1) fail("n", "must be >= 1");
+}
+
+void chain_coefficients(int kind, const qt_model_params& p, double* step, double* marg) {
+  const int n = p.steps;
+  if (kind == QT_CHAIN_BROWNIAN_1D) {
+    if (n < 1) raise(QT_ERR_NUMERIC, "BrownianChain1d: need at least one step");
+    if (!(p.horizon > 0.0)) raise(QT_ERR_NUMERIC, "BrownianChain1d: horizon must be > 0");
+  } else if (kind == QT_CHAIN_TWO_FACTOR || kind == QT_CHAIN_OU_1D) {
+    validate_params(p);
+  } else if (kind == QT_CHAIN_GBM_3D) {
+    if (n < 1) raise(QT_ERR_NUMERIC, "GbmChain3d: need at least one step");
+  } else {
+    raise(QT_ERR_INVALID_ARGUMENT, "unknown chain kind");
+  }
+  std::fill(step, step + static_cast<size_t>(n) * 6, 0.0);
+  std::fill(marg, marg + static_cast<size_t>(n + 1) * 6, 0.0);
+  if (kind == QT_CHAIN_BROWNIAN_1D) {
+    const double dt = p.horizon / n;  // dt(), chains.hpp:78
+    for (int k = 0; k < n; ++k) step[6 * k] = std::sqrt(dt);
+    for (int k = 0; k <= n; ++k) marg[6 * k] = k == 0 ? 0.0 : std::sqrt(k * dt);
+  } else if (kind == QT_CHAIN_TWO_FACTOR || kind == QT_CHAIN_OU_1D) {
+    const double dt = p.horizon / p.steps;
+    double c[3], l[3];
+    ou_cov(dt, p.alpha1, p.alpha2, p.rho, c);
+    chol2(c, l);
+    const double a1 = std::exp(-p.alpha1 * dt), a2 = std::exp(-p.alpha2 * dt);
+    for (int k = 0; k < n; ++k) {
+      double* s = step + 6 * k;
+      s[0] = a1;
+      s[1] = a2;
+      s[2] = l[0];
+      s[3] = l[1];
+      s[4] = l[2];
+    }
+    for (int k = 0; k <= n; ++k) {
+      ou_cov(k * dt, p.alpha1, p.alpha2, p.rho, c);  // marginal_cov(k), time(k) = k dt
+      chol2(c, l);
+      marg[6 * k] = l[0];
+      marg[6 * k + 1] = l[1];
+      marg[6 * k + 2] = l[2];
+    }
+  } else {
+    double L[3][3] = {{1.0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    L[1][0] = p.gbm_rho[0];
+    L[1][1] = std::sqrt(1.0 - L[1][0] * L[1][0]);
+    L[2][0] = p.gbm_rho[1];
+    L[2][1] = (p.gbm_rho[2] - L[2][0] * L[1][0]) / L[1][1];
+    L[2][2] = std::sqrt(1.0 - L[2][0] * L[2][0] - L[2][1] * L[2][1]);
+    const double dt = p.horizon / n;
+    auto fill = [&](double* o, double s) {
+      o[0] = s * L[0][0];
+      o[1] = s * L[1][0];
+      o[2] = s * L[1][1];
+      o[3] = s * L[2][0];
+      o[4] = s * L[2][1];
+      o[5] = s * L[2][2];
+    };
+    for (int k = 0; k < n; ++k) fill(step + 6 * k, std::sqrt(dt));
+    for (int k = 0; k <= n; ++k) fill(marg + 6 * k, std::sqrt(k * dt));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// grid tables
+// ---------------------------------------------------------------------------
+uint32_t round16(uint64_t b) { return static_cast<uint32_t>((b + 15) & ~uint64_t(15)); }
+
+// QuantGrid invariants (grid.hpp:24-31,41-55): finite, pairwise distinct.
+void check_grid(int dim, uint64_t npts, const double* pts, int layer) {
+  if (npts == 0) raise(QT_ERR_NUMERIC, "grid: point data size is not a positive multiple of dim");
+  for (uint64_t i = 0; i < npts * static_cast<uint64_t>(dim); ++i)
+    if (!std::isfinite(pts[i]))
+      raise(QT_ERR_NUMERIC, "grid: non-finite point coordinate (layer " + std::to_string(layer) + ")");
+  std::vector<uint32_t> ord(npts);
+  std::iota(ord.begin(), ord.end(), 0u);
+  auto less = [&](uint32_t a, uint32_t b) {
+    return std::lexicographical_compare(pts + a * dim, pts + (a + 1) * dim, pts + b * dim,
+                                        pts + (b + 1) * dim);
+  };
+  std::sort(ord.begin(), ord.end(), less);
+  for (uint64_t i = 1; i < npts; ++i)
+    if (std::equal(pts + ord[i - 1] * dim, pts + (ord[i - 1] + 1) * dim, pts + ord[i] * dim))
+      raise(QT_ERR_NUMERIC, "grid: duplicate points (layer " + std::to_string(layer) + ")");
+}
+
+// Bytes of one layer table.
+std::vector<uint8_t> build_table(int dim, uint64_t npts, const double* pts, const double* step,
+                                 const double* marg_prev, uint64_t joff, uint64_t voff,
+                                 uint64_t n_prev, uint32_t layer) {
+  LayerTable h{};
+  std::memcpy(h.step, step, sizeof h.step);
+  std::memcpy(h.marg_prev, marg_prev, sizeof h.marg_prev);
+  h.joff = joff;
+  h.voff = voff;
+  h.n_pts = static_cast<uint32_t>(npts);
+  h.n_prev = static_cast<uint32_t>(n_prev);
+  h.layer = layer;
+  h.dim = static_cast<uint32_t>(dim);
+  h.off_rec = sizeof(LayerTable);
+  std::vector<uint8_t> out;
+  if (dim == 1) {
+    std::vector<uint32_t> ord(npts);
+    std::iota(ord.begin(), ord.end(), 0u);
+    std::sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) { return pts[a] < pts[b]; });
+    std::vector<double> v(npts);
+    for (uint64_t s = 0; s < npts; ++s) v[s] = pts[ord[s]];
+    const double lo = v.front(), hi = v.back();
+    // x_safe: |x| below it rules out equal d2 between same-side neighbours
+    // (gap > 2^-51 (|x| + max|v|) suffices, 8x margin) and d2 overflow.
+    double gmin = std::numeric_limits<double>::infinity();
+    for (uint64_t s = 1; s < npts; ++s) gmin = std::min(gmin, v[s] - v[s - 1]);
+    const double vmax = std::max(std::fabs(lo), std::fabs(hi));
+    double x_safe;
+    if (npts == 1) x_safe = vmax <= 1e150 ? 1e150 : 0.0;
+    else if (gmin >= 1e-150 && vmax <= 1e150)
+      x_safe = std::min(gmin * 0x1p48 - vmax, 1e150);
+    else x_safe = 0.0;
+    if (!(x_safe > 0.0)) x_safe = 0.0;
+    if (npts > 65534) x_safe = 0.0;  // start[] is u16: exact scan only
+    // bucket count: grow until no bucket holds two points (cap 8N)
+    uint32_t nb = 1;
+    double inv_w = 0.0;
+    if (npts > 1 && npts <= 65534) {
+      for (nb = static_cast<uint32_t>(2 * npts);; nb *= 2) {
+        inv_w = static_cast<double>(nb) / (hi - lo);
+        if (!std::isfinite(inv_w)) {
+          nb = 1;
+          inv_w = 0.0;
+          break;
+        }
+        uint32_t prev = 0xFFFFFFFFu, run = 0, worst = 0;
+        for (uint64_t s = 0; s < npts; ++s) {
+          const uint32_t b = qt::bucket_of(v[s], lo, inv_w, static_cast<double>(nb), nb);
+          run = b == prev ? run + 1 : 1;
+          prev = b;
+          worst = std::max(worst, run);
+        }
+        if (worst <= 1 || nb >= 8 * npts) break;
+      }
+    }
+    h.lo = lo;
+    h.inv_w = inv_w;
+    h.x_safe = x_safe;
+    h.nb = nb;
+    h.nb_d = static_cast<double>(nb);
+    const uint64_t rec_bytes = 16ull * (npts + 2);
+    h.off_start = round16(h.off_rec + rec_bytes);
+    h.bytes = round16(h.off_start + 2ull * nb);
+    out.assign(h.bytes, 0);
+    Rec1* R = reinterpret_cast<Rec1*>(out.data() + h.off_rec);
+    R[0] = Rec1{-std::numeric_limits<double>::infinity(), qt::kNoIndex, 0};
+    for (uint64_t s = 0; s < npts; ++s) R[s + 1] = Rec1{v[s], ord[s], 0};
+    R[npts + 1] = Rec1{std::numeric_limits<double>::infinity(), qt::kNoIndex, 0};
+    uint16_t* start = reinterpret_cast<uint16_t*>(out.data() + h.off_start);
+    uint64_t s = 0;
+    for (uint32_t b = 0; b < nb; ++b) {
+      while (s < npts && qt::bucket_of(v[s], lo, inv_w, h.nb_d, nb) < b) ++s;
+      start[b] = static_cast<uint16_t>(std::min<uint64_t>(s, 65535));
+    }
+  } else {
+    h.bytes = round16(h.off_rec + 8ull * dim * npts);
+    out.assign(h.bytes, 0);
+    std::memcpy(out.data() + h.off_rec, pts, 8ull * dim * npts);
+  }
+  std::memcpy(out.data(), &h, sizeof h);
+  return out;
+}
+
+constexpr uint32_t kMaxTableBytes = 110u * 1024u;  // two must fit in 227 KB of smem
+constexpr uint32_t kResidentBudget = 96u * 1024u;
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+struct qt_plan {
+  int device = 0;
+  int kind = 0, dim = 1, nps = 1, n = 0;
+  std::vector<uint64_t> sizes, voff, joff;
+  uint64_t nvis = 0, njoint = 0, max_cols = 0, max_rows = 0, max_elems = 0;
+  std::vector<uint32_t> tab_off, tab_bytes;
+  uint32_t max_tab = 0, total_tab = 0;
+  int sm_count = 148;
+  uint8_t* d_tables = nullptr;
+  uint32_t* d_tab_off = nullptr;
+  uint32_t* d_tab_bytes = nullptr;
+  uint64_t* d_fin = nullptr;  // rows, cols, joff, voff_row, voff_col (5 x n)
+  std::vector<uint8_t> host_tables;
+
+  ~qt_plan() {
+    cudaSetDevice(device);
+    cudaFree(d_tables);
+    cudaFree(d_tab_off);
+    cudaFree(d_tab_bytes);
+    cudaFree(d_fin);
+  }
+};
+
+namespace {
+
+void check_inputs(const qt_chain* chain, const qt_grids* grids) {
+  if (!chain || !grids || !grids->sizes || !grids->points || !chain->step || !chain->marginal)
+    raise(QT_ERR_INVALID_ARGUMENT, "estimate: null argument");
+  const int dim = chain_dim(chain->kind);
+  if (grids->layers != chain->layers || chain->layers < 1)
+    raise(QT_ERR_INVALID_ARGUMENT, "estimate: need one grid per layer 1..n");
+  if (grids->dim != dim) raise(QT_ERR_INVALID_ARGUMENT, "estimate: grid dimension mismatch");
+  if (grids->sizes[0] != 1) raise(QT_ERR_INVALID_ARGUMENT, "estimate: layer 0 must be {x0}");
+}
+
+qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
+  check_inputs(chain, grids);
+  auto p = std::make_unique<qt_plan>();
+  p->device = device;
+  p->kind = chain->kind;
+  p->dim = chain_dim(chain->kind);
+  p->nps = p->dim;
+  p->n = chain->layers;
+  const int n = p->n;
+  p->sizes.assign(grids->sizes, grids->sizes + n + 1);
+  p->voff.assign(n + 2, 0);
+  p->joff.assign(n + 1, 0);
+  for (int k = 0; k <= n; ++k) p->voff[k + 1] = p->voff[k] + p->sizes[k];
+  for (int t = 0; t < n; ++t) {
+    p->joff[t + 1] = p->joff[t] + p->sizes[t] * p->sizes[t + 1];
+    p->max_cols = std::max(p->max_cols, p->sizes[t + 1]);
+    p->max_rows = std::max(p->max_rows, p->sizes[t]);
+    p->max_elems = std::max(p->max_elems, p->sizes[t] * p->sizes[t + 1]);
+  }
+  p->nvis = p->voff[n + 1];
+  p->njoint = p->joff[n];
+  // tables
+  const double* pts = grids->points;
+  for (int k = 1; k <= n; ++k) {
+    const uint64_t N = p->sizes[k];
+    if (N == 0 || N > 0xFFFFFFF0ull)
+      raise(QT_ERR_NUMERIC, "grid: point data size is not a positive multiple of dim");
+    check_grid(p->dim, N, pts, k);
+    auto t = build_table(p->dim, N, pts, chain->step + 6 * (k - 1), chain->marginal + 6 * (k - 1),
+                         p->joff[k - 1], p->voff[k], p->sizes[k - 1], static_cast<uint32_t>(k));
+    if (t.size() > kMaxTableBytes)
+      raise(QT_ERR_INVALID_ARGUMENT,
+            "estimate: layer " + std::to_string(k) + " grid table (" + std::to_string(t.size()) +
+                " B) exceeds the shared-memory staging limit");
+    p->tab_off.push_back(static_cast<uint32_t>(p->host_tables.size()));
+    p->tab_bytes.push_back(static_cast<uint32_t>(t.size()));
+    p->max_tab = std::max<uint32_t>(p->max_tab, static_cast<uint32_t>(t.size()));
+    p->host_tables.insert(p->host_tables.end(), t.begin(), t.end());
+    pts += N * p->dim;
+  }
+  p->total_tab = static_cast<uint32_t>(p->host_tables.size());
+  QT_CUDA(cudaSetDevice(device));
+  QT_CUDA(cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, device));
+  QT_CUDA(cudaMalloc(&p->d_tables, p->host_tables.size()));
+  QT_CUDA(cudaMemcpy(p->d_tables, p->host_tables.data(), p->host_tables.size(),
+                     cudaMemcpyHostToDevice));
+  QT_CUDA(cudaMalloc(&p->d_tab_off, n * sizeof(uint32_t)));
+  QT_CUDA(cudaMalloc(&p->d_tab_bytes, n * sizeof(uint32_t)));
+  QT_CUDA(cudaMemcpy(p->d_tab_off, p->tab_off.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  QT_CUDA(cudaMemcpy(p->d_tab_bytes, p->tab_bytes.data(), n * sizeof(uint32_t),
+                     cudaMemcpyHostToDevice));
+  std::vector<uint64_t> fin(5 * n);
+  for (int t = 0; t < n; ++t) {
+    fin[t] = p->sizes[t];
+    fin[n + t] = p->sizes[t + 1];
+    fin[2 * n + t] = p->joff[t];
+    fin[3 * n + t] = p->voff[t];
+    fin[4 * n + t] = p->voff[t + 1];
+  }
+  QT_CUDA(cudaMalloc(&p->d_fin, fin.size() * sizeof(uint64_t)));
+  QT_CUDA(cudaMemcpy(p->d_fin, fin.data(), fin.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  device_tables(device);
+  return p.release();
+}
+
+int source_of(int engine, bool normals_in) {
+  if (normals_in) return 3;
+  if (engine < 0 || engine > 2) raise(QT_ERR_INVALID_ARGUMENT, "unknown engine kind");
+  return engine;
+}
+
+// Enqueue the count kernel(s) for units [first, first+count).
+int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, uint64_t count,
+               uint64_t total, const double* d_normals, uint64_t* d_joint, cudaStream_t st) {
+  if (alg < QT_ALG_I || alg > QT_ALG_III)
+    raise(QT_ERR_INVALID_ARGUMENT, "estimate: unknown estimator kind");
+  if (count == 0) return 0;
+  QT_CUDA(cudaSetDevice(p->device));
+  const int src = source_of(engine, d_normals != nullptr);
+  const int launches_before = 0;
+  if (alg != QT_ALG_III) {
+    const uint64_t normals = static_cast<uint64_t>(p->n) * p->nps;
+    qt::PathArgs a{};
+    a.src = make_src(p->device, engine, seed, 2 * ((normals + 1) / 2),
+                     static_cast<uint32_t>(normals), d_normals, first);
+    a.tables = p->d_tables;
+    a.tab_off = p->d_tab_off;
+    a.tab_bytes = p->d_tab_bytes;
+    a.joint = reinterpret_cast<unsigned long long*>(d_joint);
+    a.first = first;
+    a.n = static_cast<uint32_t>(p->n);
+    a.buf_bytes = p->max_tab;
+    a.resident_bytes = p->total_tab;
+    const bool resident = p->total_tab <= kResidentBudget;
+    const size_t smem = resident ? p->total_tab : 2ull * p->max_tab;
+    const int bps = qt::paths_blocks_per_sm(p->kind, src, resident, smem);
+    uint64_t blocks = static_cast<uint64_t>(p->sm_count) * bps;
+    const uint64_t need = (count + 255) / 256;
+    if (need < blocks) blocks = need;
+    const uint64_t T = blocks * 256;
+    a.q = count / T;
+    a.rem = count % T;
+    QT_CUDA(qt::launch_paths(p->kind, src, resident, a, static_cast<uint32_t>(blocks), smem, st));
+  } else {
+    if (total % p->n != 0) raise(QT_ERR_INVALID_ARGUMENT, "Alg III: total must be n * M");
+    const uint64_t M = total / p->n;
+    qt::Alg3Args a{};
+    const uint64_t normals = static_cast<uint64_t>(p->dim) + p->nps;
+    a.src = make_src(p->device, engine, seed, 2 * ((normals + 1) / 2),
+                     static_cast<uint32_t>(normals), d_normals, first);
+    a.tables = p->d_tables;
+    a.tab_off = p->d_tab_off;
+    a.tab_bytes = p->d_tab_bytes;
+    a.joint = reinterpret_cast<unsigned long long*>(d_joint);
+    a.M = M;
+    a.first = first;
+    a.count = count;
+    a.n = static_cast<uint32_t>(p->n);
+    a.buf_bytes = p->max_tab;
+    const size_t smem = 2ull * p->max_tab;
+    // slices per layer: ~8 waves of resident CTAs overall, >= 64 samples per thread
+    uint64_t slices = std::max<uint64_t>(1, (static_cast<uint64_t>(p->sm_count) * 32) / p->n);
+    const uint64_t cap = std::max<uint64_t>(1, M / (256 * 64));
+    slices = std::min(slices, cap);
+    slices = std::min<uint64_t>(slices, 1u << 30);
+    QT_CUDA(qt::launch_alg3(p->kind, src, a, static_cast<uint32_t>(slices), smem, st));
+  }
+  g_launches.fetch_add(1);
+  return 1 + launches_before;
+}
+
+int plan_finalize(qt_plan* p, int alg, uint64_t samples, const uint64_t* d_joint, uint64_t* d_visits,
+                  double* d_pi, cudaStream_t st) {
+  QT_CUDA(cudaSetDevice(p->device));
+  const int n = p->n;
+  qt::FinalizeArgs f{p->d_fin, p->d_fin + n, p->d_fin + 2 * n, p->d_fin + 3 * n, p->d_fin + 4 * n};
+  int l = 0;
+  QT_CUDA(qt::launch_finalize(alg == QT_ALG_III, reinterpret_cast<const unsigned long long*>(d_joint),
+                              reinterpret_cast<unsigned long long*>(d_visits), d_pi, samples, f,
+                              static_cast<uint32_t>(n), p->max_cols, p->max_rows, p->max_elems, st,
+                              &l));
+  g_launches.fetch_add(static_cast<uint64_t>(l));
+  return l;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded on demand (only multi-device calls need it)
+// ---------------------------------------------------------------------------
+struct Nccl {
+  typedef int (*InitAll)(void** comms, int ndev, const int* devlist);
+  typedef int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+  typedef int (*Group)();
+  typedef int (*Destroy)(void*);
+  typedef const char* (*ErrStr)(int);
+  InitAll init_all = nullptr;
+  AllReduce all_reduce = nullptr;
+  Group group_start = nullptr, group_end = nullptr;
+  Destroy destroy = nullptr;
+  ErrStr err = nullptr;
+  bool ok = false;
+};
+
+const Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    n.init_all = reinterpret_cast<Nccl::InitAll>(dlsym(h, "ncclCommInitAll"));
+    n.all_reduce = reinterpret_cast<Nccl::AllReduce>(dlsym(h, "ncclAllReduce"));
+    n.group_start = reinterpret_cast<Nccl::Group>(dlsym(h, "ncclGroupStart"));
+    n.group_end = reinterpret_cast<Nccl::Group>(dlsym(h, "ncclGroupEnd"));
+    n.destroy = reinterpret_cast<Nccl::Destroy>(dlsym(h, "ncclCommDestroy"));
+    n.err = reinterpret_cast<Nccl::ErrStr>(dlsym(h, "ncclGetErrorString"));
+    n.ok = n.init_all && n.all_reduce && n.group_start && n.group_end && n.destroy;
+  });
+  return n;
+}
+constexpr int kNcclUint64 = 5;  // ncclUint64
+constexpr int kNcclSum = 0;     // ncclSum
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// Shared body of qt_estimate / qt_estimate_normals / qt_accumulate_paths.
+void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_t samples,
+                  int engine, uint64_t seed, int devices, const double* h_normals,
+                  uint64_t win_first, uint64_t win_count, uint64_t win_total, bool accumulate,
+                  uint64_t* visits, uint64_t* joint, double* pi, double* phases) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (alg < QT_ALG_I || alg > QT_ALG_III)
+    raise(QT_ERR_INVALID_ARGUMENT, "estimate: unknown estimator kind");
+  if (samples == 0) raise(QT_ERR_INVALID_ARGUMENT, "estimate: need at least one path");
+  if (devices < 1) raise(QT_ERR_INVALID_ARGUMENT, "estimate: devices must be >= 1");
+  int avail = 0;
+  if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+    raise(QT_ERR_DEVICE, "cuda: no CUDA device available (the estimator has no CPU path)");
+  if (devices > avail)
+    raise(QT_ERR_INVALID_ARGUMENT, "estimate: requested " + std::to_string(devices) +
+                                       " devices, " + std::to_string(avail) + " present");
+  if (h_normals && devices != 1) raise(QT_ERR_INVALID_ARGUMENT, "normals mode is single-device");
+  check_inputs(chain, grids);
+  const int n = chain->layers;
+  const uint64_t units_total = alg == QT_ALG_III ? static_cast<uint64_t>(n) * samples : samples;
+  const uint64_t first = accumulate ? win_first : 0;
+  const uint64_t count = accumulate ? win_count : units_total;
+  const uint64_t total = accumulate ? win_total : units_total;
+  const int G = devices;
+  std::vector<std::unique_ptr<qt_plan>> plans(G);
+  std::vector<uint64_t*> dj(G, nullptr);
+  std::vector<cudaStream_t> streams(G, nullptr);
+  std::vector<cudaEvent_t> ev(4 * G, nullptr);
+  double* d_normals = nullptr;
+  uint64_t* d_vis = nullptr;
+  double* d_pi = nullptr;
+  auto cleanup = [&] {
+    for (int g = 0; g < G; ++g) {
+      cudaSetDevice(g);
+      if (dj[g]) cudaFree(dj[g]);
+      if (streams[g]) cudaStreamDestroy(streams[g]);
+      for (int e = 0; e < 4; ++e)
+        if (ev[4 * g + e]) cudaEventDestroy(ev[4 * g + e]);
+    }
+    cudaSetDevice(0);
+    cudaFree(d_normals);
+    cudaFree(d_vis);
+    cudaFree(d_pi);
+  };
+  try {
+    for (int g = 0; g < G; ++g) {
+      plans[g].reset(make_plan(chain, grids, g));
+      QT_CUDA(cudaSetDevice(g));
+      QT_CUDA(cudaStreamCreateWithFlags(&streams[g], cudaStreamNonBlocking));
+      for (int e = 0; e < 4; ++e) QT_CUDA(cudaEventCreate(&ev[4 * g + e]));
+      QT_CUDA(cudaMalloc(&dj[g], plans[g]->njoint * sizeof(uint64_t)));
+      QT_CUDA(cudaMemsetAsync(dj[g], 0, plans[g]->njoint * sizeof(uint64_t), streams[g]));
+    }
+    if (h_normals) {
+      const uint64_t per = alg == QT_ALG_III ? static_cast<uint64_t>(plans[0]->dim + plans[0]->nps)
+                                             : static_cast<uint64_t>(n) * plans[0]->nps;
+      QT_CUDA(cudaSetDevice(0));
+      QT_CUDA(cudaMalloc(&d_normals, count * per * sizeof(double)));
+      QT_CUDA(cudaMemcpyAsync(d_normals, h_normals, count * per * sizeof(double),
+                              cudaMemcpyHostToDevice, streams[0]));
+    }
+    // shard g: units [first + count g / G, first + count (g+1) / G)  (estimate.hpp:180-181)
+    for (int g = 0; g < G; ++g) {
+      const uint64_t b = first + static_cast<uint64_t>(static_cast<u128>(count) * g / G);
+      const uint64_t e = first + static_cast<uint64_t>(static_cast<u128>(count) * (g + 1) / G);
+      QT_CUDA(cudaSetDevice(g));
+      QT_CUDA(cudaEventRecord(ev[4 * g], streams[g]));
+      plan_count(plans[g].get(), alg, engine, seed, b, e - b, total, d_normals, dj[g], streams[g]);
+      QT_CUDA(cudaEventRecord(ev[4 * g + 1], streams[g]));
+    }
+    if (G > 1) {
+      const Nccl& nc = nccl();
+      if (!nc.ok) raise(QT_ERR_DEVICE, "nccl: libnccl.so.2 not loadable for devices > 1");
+      std::vector<void*> comms(G);
+      std::vector<int> devs(G);
+      std::iota(devs.begin(), devs.end(), 0);
+      int rc = nc.init_all(comms.data(), G, devs.data());
+      if (rc) raise(QT_ERR_DEVICE, std::string("nccl: ") + (nc.err ? nc.err(rc) : "init failed"));
+      nc.group_start();
+      for (int g = 0; g < G; ++g) {
+        cudaSetDevice(g);
+        nc.all_reduce(dj[g], dj[g], plans[g]->njoint, kNcclUint64, kNcclSum, comms[g], streams[g]);
+      }
+      rc = nc.group_end();
+      for (int g = 0; g < G; ++g) {
+        cudaSetDevice(g);
+        cudaEventRecord(ev[4 * g + 2], streams[g]);
+        cudaStreamSynchronize(streams[g]);
+        nc.destroy(comms[g]);
+      }
+      if (rc) raise(QT_ERR_DEVICE, std::string("nccl: ") + (nc.err ? nc.err(rc) : "all-reduce failed"));
+    } else {
+      QT_CUDA(cudaEventRecord(ev[2], streams[0]));
+    }
+    QT_CUDA(cudaSetDevice(0));
+    qt_plan* p0 = plans[0].get();
+    QT_CUDA(cudaMalloc(&d_vis, p0->nvis * sizeof(uint64_t)));
+    const uint64_t M_for_visits = accumulate ? count : samples;
+    if (!accumulate) QT_CUDA(cudaMalloc(&d_pi, p0->njoint * sizeof(double)));
+    else QT_CUDA(cudaMalloc(&d_pi, p0->njoint * sizeof(double)));
+    plan_finalize(p0, alg, M_for_visits, dj[0], d_vis, d_pi, streams[0]);
+    QT_CUDA(cudaEventRecord(ev[3], streams[0]));
+    std::vector<uint64_t> hv, hj;
+    if (accumulate) {
+      hv.resize(p0->nvis);
+      hj.resize(p0->njoint);
+      QT_CUDA(cudaMemcpyAsync(hv.data(), d_vis, p0->nvis * 8, cudaMemcpyDeviceToHost, streams[0]));
+      QT_CUDA(cudaMemcpyAsync(hj.data(), dj[0], p0->njoint * 8, cudaMemcpyDeviceToHost, streams[0]));
+    } else {
+      QT_CUDA(cudaMemcpyAsync(visits, d_vis, p0->nvis * 8, cudaMemcpyDeviceToHost, streams[0]));
+      QT_CUDA(cudaMemcpyAsync(joint, dj[0], p0->njoint * 8, cudaMemcpyDeviceToHost, streams[0]));
+      if (pi)
+        QT_CUDA(cudaMemcpyAsync(pi, d_pi, p0->njoint * 8, cudaMemcpyDeviceToHost, streams[0]));
+    }
+    QT_CUDA(cudaStreamSynchronize(streams[0]));
+    if (accumulate) {
+      for (uint64_t i = 0; i < p0->nvis; ++i) visits[i] += hv[i];
+      for (uint64_t i = 0; i < p0->njoint; ++i) joint[i] += hj[i];
+    }
+    if (phases) {
+      float count_ms = 0, merge_ms = 0, norm_ms = 0;
+      for (int g = 0; g < G; ++g) {
+        float c = 0;
+        cudaSetDevice(g);
+        cudaEventElapsedTime(&c, ev[4 * g], ev[4 * g + 1]);
+        count_ms = std::max(count_ms, c);
+      }
+      cudaSetDevice(0);
+      cudaEventElapsedTime(&merge_ms, ev[1], ev[2]);
+      cudaEventElapsedTime(&norm_ms, ev[2], ev[3]);
+      phases[0] = 0.0;       // simulate: fused into the path kernel, reported under nn
+      phases[1] = count_ms;  // fused path kernel (busiest device)
+      phases[2] = merge_ms;  // NCCL all-reduce
+      phases[3] = norm_ms;   // visits + normalize
+      phases[4] = ms_since(t0);
+    }
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+
+}  // namespace
+
+namespace qt {
+void note_error(const std::string& msg) { g_error = msg; }
+void note_launches(uint64_t n) { g_launches.fetch_add(n); }
+}  // namespace qt
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+QT_API qt_status qt_chain_coefficients(int32_t kind, const qt_model_params* params, double* step,
+                                       double* marginal) {
+  return guarded([&] {
+    if (!params || !step || !marginal) raise(QT_ERR_INVALID_ARGUMENT, "null argument");
+    chain_coefficients(kind, *params, step, marginal);
+  });
+}
+
+QT_API qt_status qt_estimate(int32_t estimator, const qt_chain* chain, const qt_grids* grids,
+                             uint64_t samples, int32_t engine, uint64_t seed, int32_t devices,
+                             uint64_t* visits, uint64_t* joint, double* pi, double* phases_ms) {
+  return guarded([&] {
+    if (!visits || !joint) raise(QT_ERR_INVALID_ARGUMENT, "estimate: null output");
+    source_of(engine, false);
+    run_estimate(estimator, chain, grids, samples, engine, seed, devices, nullptr, 0, 0, 0, false,
+                 visits, joint, pi, phases_ms);
+  });
+}
+
+QT_API qt_status qt_estimate_normals(int32_t estimator, const qt_chain* chain,
+                                     const qt_grids* grids, uint64_t samples,
+                                     const double* normals, uint64_t* visits, uint64_t* joint,
+                                     double* pi) {
+  return guarded([&] {
+    if (!visits || !joint || !normals) raise(QT_ERR_INVALID_ARGUMENT, "estimate: null argument");
+    run_estimate(estimator, chain, grids, samples, QT_ENGINE_MRG32K3A, 0, 1, normals, 0, 0, 0,
+                 false, visits, joint, pi, nullptr);
+  });
+}
+
+QT_API qt_status qt_accumulate_paths(const qt_chain* chain, const qt_grids* grids,
+                                     int32_t engine, uint64_t seed, uint64_t first,
+                                     uint64_t count, uint64_t total, uint64_t* visits,
+                                     uint64_t* joint) {
+  return guarded([&] {
+    if (!visits || !joint) raise(QT_ERR_INVALID_ARGUMENT, "accumulate: null output");
+    source_of(engine, false);
+    if (count == 0) return;
+    run_estimate(QT_ALG_I, chain, grids, total ? total : 1, engine, seed, 1, nullptr, first,
+                 count, total, true, visits, joint, nullptr, nullptr);
+  });
+}
+
+QT_API qt_status qt_plan_create(const qt_chain* chain, const qt_grids* grids, int32_t device,
+                                qt_plan** out) {
+  return guarded([&] {
+    if (!out) raise(QT_ERR_INVALID_ARGUMENT, "plan: null output");
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+      raise(QT_ERR_DEVICE, "cuda: no CUDA device available (the estimator has no CPU path)");
+    if (device < 0 || device >= avail) raise(QT_ERR_INVALID_ARGUMENT, "plan: bad device");
+    *out = make_plan(chain, grids, device);
+  });
+}
+
+QT_API qt_status qt_plan_destroy(qt_plan* plan) {
+  return guarded([&] { delete plan; });
+}
+
+QT_API qt_status qt_plan_layout(const qt_plan* plan, uint64_t* n_visits, uint64_t* n_joint) {
+  return guarded([&] {
+    if (!plan) raise(QT_ERR_INVALID_ARGUMENT, "plan: null");
+    if (n_visits) *n_visits = plan->nvis;
+    if (n_joint) *n_joint = plan->njoint;
+  });
+}
+
+QT_API qt_status qt_plan_count(qt_plan* plan, int32_t estimator, int32_t engine, uint64_t seed,
+                               uint64_t first, uint64_t count, uint64_t total,
+                               const double* d_normals, uint64_t* d_joint, void* stream,
+                               int32_t* launches) {
+  return guarded([&] {
+    if (!plan || !d_joint) raise(QT_ERR_INVALID_ARGUMENT, "plan_count: null argument");
+    if (total == 0 || first + count > total)
+      raise(QT_ERR_INVALID_ARGUMENT, "plan_count: window outside [0, total)");
+    const int l = plan_count(plan, estimator, engine, seed, first, count, total, d_normals, d_joint,
+                             static_cast<cudaStream_t>(stream));
+    if (launches) *launches = l;
+  });
+}
+
+QT_API qt_status qt_plan_finalize(qt_plan* plan, int32_t estimator, uint64_t samples,
+                                  const uint64_t* d_joint, uint64_t* d_visits, double* d_pi,
+                                  void* stream, int32_t* launches) {
+  return guarded([&] {
+    if (!plan || !d_joint || !d_visits || !d_pi)
+      raise(QT_ERR_INVALID_ARGUMENT, "plan_finalize: null argument");
+    if (estimator < QT_ALG_I || estimator > QT_ALG_III)
+      raise(QT_ERR_INVALID_ARGUMENT, "estimate: unknown estimator kind");
+    const int l = plan_finalize(plan, estimator, samples, d_joint, d_visits, d_pi,
+                                static_cast<cudaStream_t>(stream));
+    if (launches) *launches = l;
+  });
+}
+
+QT_API qt_status qt_nearest(int32_t dim, uint64_t n_points, const double* points,
+                            uint64_t n_queries, const double* queries, uint64_t* out) {
+  return guarded([&] {
+    if (dim < 1 || dim > 3) raise(QT_ERR_INVALID_ARGUMENT, "nearest: dimension must be 1..3");
+    if (!points || (!queries && n_queries) || (!out && n_queries))
+      raise(QT_ERR_INVALID_ARGUMENT, "nearest: null argument");
+    check_grid(dim, n_points, points, 0);
+    if (n_queries == 0) return;
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+      raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
+    double zeros[6] = {0, 0, 0, 0, 0, 0};
+    auto t = build_table(dim, n_points, points, zeros, zeros, 0, 0, 1, 1);
+    QT_CUDA(cudaSetDevice(0));
+    uint8_t* d_t = nullptr;
+    double* d_q = nullptr;
+    unsigned long long* d_o = nullptr;
+    auto fin = [&] {
+      cudaFree(d_t);
+      cudaFree(d_q);
+      cudaFree(d_o);
+    };
+    try {
+      QT_CUDA(cudaMalloc(&d_t, t.size()));
+      QT_CUDA(cudaMalloc(&d_q, n_queries * dim * sizeof(double)));
+      QT_CUDA(cudaMalloc(&d_o, n_queries * sizeof(uint64_t)));
+      QT_CUDA(cudaMemcpy(d_t, t.data(), t.size(), cudaMemcpyHostToDevice));
+      QT_CUDA(cudaMemcpy(d_q, queries, n_queries * dim * sizeof(double), cudaMemcpyHostToDevice));
+      QT_CUDA(qt::launch_nearest(dim, d_t, static_cast<uint32_t>(t.size()), d_q, n_queries, d_o,
+                                 nullptr));
+      g_launches.fetch_add(1);
+      QT_CUDA(cudaMemcpy(out, d_o, n_queries * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    } catch (...) {
+      fin();
+      throw;
+    }
+    fin();
+  });
+}
+
+QT_API qt_status qt_path_normals(int32_t engine, uint64_t seed, uint64_t normals_per_path,
+                                 uint64_t first, uint64_t count, double* out) {
+  return guarded([&] {
+    source_of(engine, false);
+    if (count == 0) return;
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+      raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
+    QT_CUDA(cudaSetDevice(0));
+    auto a = make_src(0, engine, seed, 2 * ((normals_per_path + 1) / 2),
+                      static_cast<uint32_t>(normals_per_path), nullptr, 0);
+    double* d = nullptr;
+    QT_CUDA(cudaMalloc(&d, count * normals_per_path * sizeof(double)));
+    cudaError_t e = qt::launch_path_normals(engine, a, first, count, d, nullptr);
+    g_launches.fetch_add(1);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(out, d, count * normals_per_path * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    QT_CUDA(e);
+  });
+}
+
+QT_API qt_status qt_uniforms(int32_t engine, uint64_t seed, uint64_t offset, uint64_t count,
+                             double* out) {
+  return guarded([&] {
+    if (engine != QT_ENGINE_MRG32K3A && engine != QT_ENGINE_LCG48)
+      raise(QT_ERR_INVALID_ARGUMENT, "uniforms: jumpable engines only");
+    if (count == 0) return;
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+      raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
+    QT_CUDA(cudaSetDevice(0));
+    auto a = make_src(0, engine, seed, 1, 1, nullptr, 0);
+    double* d = nullptr;
+    QT_CUDA(cudaMalloc(&d, count * sizeof(double)));
+    cudaError_t e = qt::launch_uniforms(engine, a, offset, count, d, nullptr);
+    g_launches.fetch_add(1);
+    if (e == cudaSuccess) e = cudaMemcpy(out, d, count * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    QT_CUDA(e);
+  });
+}
+
+QT_API const char* qt_last_error(void) { return g_error.c_str(); }
+
+QT_API const char* qt_version(void) {
+  return "qtree_cuda 0.1 sm_100a (fused MRG32k3a/LCG48/XORWOW path kernel, cp.async.bulk tables)";
+}
+
+QT_API uint64_t qt_kernel_launches(void) { return g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,525 @@
+// qt_device.cuh -- device building blocks of the fused path kernel:
+// the three reference RNG engines with O(log s) positioning, Box-Muller,
+// the chain steps, the exact Voronoi projection and the async-copy helpers.
+//
+// Every floating-point expression that mirrors reference arithmetic uses the
+// explicitly rounded intrinsics (__dadd_rn / __dsub_rn / __dmul_rn), which the
+// compiler never contracts into FMA: the reference is built without FMA
+// contraction (SURVEY.md §7 hard part 1), and bit-exact cell indices need every
+// product and sum rounded exactly as it rounds there.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qt_internal.h"
+#include "qt_layout.h"
+
+namespace qt {
+
+// ---------------------------------------------------------------------------
+// MRG32k3a (rng/mrg32k3a.hpp:8-63). State words are residues < 2^32, kept in
+// u32 registers; each recurrence is one 32x32->64 multiply-add pair plus a
+// two-fold reduction by 2^32 = m + c, which yields the same residue as the
+// reference's signed-64 `%` + fix-up.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kM1 = 4294967087u;
+constexpr uint32_t kM2 = 4294944443u;
+constexpr uint32_t kC1 = 209u;    // 2^32 - m1
+constexpr uint32_t kC2 = 22853u;  // 2^32 - m2
+constexpr uint32_t kA12 = 1403580u, kA13n = 810728u, kA21 = 527612u, kA23n = 1370589u;
+// (double)(m1 + 1): the uniform is (x + 1) / (m1 + 1), mrg32k3a.hpp:62
+constexpr double kM1p1 = 4294967088.0;
+constexpr double kInvM1p1 = 1.0 / 4294967088.0;
+
+struct Mrg {
+  uint32_t a0, a1, a2;  // s1 = (x_{n-3}, x_{n-2}, x_{n-1})
+  uint32_t b0, b1, b2;  // s2
+};
+
+__device__ __forceinline__ uint64_t mulw(uint32_t a, uint32_t b) {
+  return static_cast<uint64_t>(a) * static_cast<uint64_t>(b);
+}
+
+// t mod m1 for any t < 2^64
+__device__ __forceinline__ uint32_t red_m1(uint64_t t) {
+  uint64_t r = mulw(static_cast<uint32_t>(t >> 32), kC1) + (t & 0xffffffffull);
+  r = mulw(static_cast<uint32_t>(r >> 32), kC1) + (r & 0xffffffffull);
+  return static_cast<uint32_t>(r >= kM1 ? r - kM1 : r);
+}
+// t mod m2 for any t < 2^64
+__device__ __forceinline__ uint32_t red_m2(uint64_t t) {
+  uint64_t r = mulw(static_cast<uint32_t>(t >> 32), kC2) + (t & 0xffffffffull);
+  r = mulw(static_cast<uint32_t>(r >> 32), kC2) + (r & 0xffffffffull);
+  return static_cast<uint32_t>(r >= kM2 ? r - kM2 : r);
+}
+
+// One step of both recurrences; returns the combined integer x in [0, m1).
+__device__ __forceinline__ uint32_t mrg_step(Mrg& s) {
+  // p1 = (a12 s1[1] - a13n s1[0]) mod m1, made non-negative by + a13n m1
+  const uint32_t p1 = red_m1(mulw(kA12, s.a1) + mulw(kA13n, kM1 - s.a0));
+  s.a0 = s.a1;
+  s.a1 = s.a2;
+  s.a2 = p1;
+  // p2 = (a21 s2[2] - a23n s2[0]) mod m2
+  const uint32_t p2 = red_m2(mulw(kA21, s.b2) + mulw(kA23n, kM2 - s.b0));
+  s.b0 = s.b1;
+  s.b1 = s.b2;
+  s.b2 = p2;
+  return p1 >= p2 ? p1 - p2 : p1 - p2 + kM1;  // mod-2^32 wrap gives the exact value
+}
+
+// (x + 1) / (m1 + 1), correctly rounded. Division by the constant is done as
+// q = RN(a R); r = a - q d (exact, FMA); RN(q + r R): tests/test_division.py
+// proves it equals the IEEE quotient for all 2^32 possible numerators.
+__device__ __forceinline__ double mrg_to_unit(uint32_t x) {
+  const double a = __uint2double_rn(x + 1u);
+#if defined(QT_PLAIN_DIVISION)
+  return __ddiv_rn(a, kM1p1);
+#else
+  const double q = __dmul_rn(a, kInvM1p1);
+  const double r = __fma_rn(-q, kM1p1, a);
+  return __fma_rn(r, kInvM1p1, q);
+#endif
+}
+
+// 3x3 matrix (mod m) times state; the jump table holds J^(2^b) for b = 0..63
+// (rows of u32 residues, [b][component][3][3]).
+__device__ __forceinline__ void mat_apply_m1(const uint32_t* J, uint32_t& x0, uint32_t& x1,
+                                             uint32_t& x2) {
+  uint32_t r[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const uint64_t acc = static_cast<uint64_t>(red_m1(mulw(__ldg(J + 3 * i + 0), x0))) +
+                         red_m1(mulw(__ldg(J + 3 * i + 1), x1)) +
+                         red_m1(mulw(__ldg(J + 3 * i + 2), x2));
+    r[i] = red_m1(acc);
+  }
+  x0 = r[0];
+  x1 = r[1];
+  x2 = r[2];
+}
+__device__ __forceinline__ void mat_apply_m2(const uint32_t* J, uint32_t& x0, uint32_t& x1,
+                                             uint32_t& x2) {
+  uint32_t r[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const uint64_t acc = static_cast<uint64_t>(red_m2(mulw(__ldg(J + 3 * i + 0), x0))) +
+                         red_m2(mulw(__ldg(J + 3 * i + 1), x1)) +
+                         red_m2(mulw(__ldg(J + 3 * i + 2), x2));
+    r[i] = red_m2(acc);
+  }
+  x0 = r[0];
+  x1 = r[1];
+  x2 = r[2];
+}
+
+// state <- J^e state (mrg32k3a_skip, mrg32k3a.hpp:124-146), O(log e)
+__device__ __forceinline__ void mrg_jump(Mrg& s, uint64_t e, const uint32_t* table) {
+  for (int b = 0; e != 0; ++b, e >>= 1) {
+    if (e & 1ull) {
+      mat_apply_m1(table + b * 18, s.a0, s.a1, s.a2);
+      mat_apply_m2(table + b * 18 + 9, s.b0, s.b1, s.b2);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// LCG48 (rng/lcg48.hpp): x <- a x + c mod 2^48, u = x 2^-48. Jump table holds
+// the affine maps of 2^b steps, [b] = (A, C).
+// ---------------------------------------------------------------------------
+constexpr uint64_t kLcgMask = (1ull << 48) - 1;
+constexpr uint64_t kLcgA = 0x5DEECE66Dull;
+constexpr uint64_t kLcgC = 0xBull;
+
+__device__ __forceinline__ double lcg_uniform(uint64_t& x) {
+  x = (kLcgA * x + kLcgC) & kLcgMask;
+  return __ull2double_rn(x) * 0x1p-48;
+}
+
+__device__ __forceinline__ void lcg_jump(uint64_t& x, uint64_t e, const unsigned long long* table) {
+  for (int b = 0; e != 0; ++b, e >>= 1)
+    if (e & 1ull) x = (__ldg(table + 2 * b) * x + __ldg(table + 2 * b + 1)) & kLcgMask;
+}
+
+// ---------------------------------------------------------------------------
+// XORWOW (rng/xorwow.hpp:16-47), re-seeded per path with 64 burn-in steps
+// (stream.hpp:146-153,207-209).
+// ---------------------------------------------------------------------------
+struct Xorwow {
+  uint32_t v, w, x, y, z, d;
+};
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t& z) {
+  z += 0x9E3779B97F4A7C15ull;
+  uint64_t v = z;
+  v = (v ^ (v >> 30)) * 0xBF58476D1CE4E5B9ull;
+  v = (v ^ (v >> 27)) * 0x94D049BB133111EBull;
+  return v ^ (v >> 31);
+}
+
+__device__ __forceinline__ uint32_t xorwow_step(Xorwow& s) {
+  const uint32_t t = s.x ^ (s.x >> 2);
+  s.x = s.y;
+  s.y = s.z;
+  s.z = s.w;
+  s.w = s.v;
+  s.v = (s.v ^ (s.v << 4)) ^ (t ^ (t << 1));
+  s.d += 362437u;
+  return s.v + s.d;
+}
+
+__device__ __forceinline__ Xorwow xorwow_stream(uint64_t seed, uint64_t stream) {
+  uint64_t z = seed ^ (0x9E3779B97F4A7C15ull * (stream + 1));
+  const uint64_t a = splitmix64(z), b = splitmix64(z), c = splitmix64(z);
+  Xorwow s{static_cast<uint32_t>(a), static_cast<uint32_t>(a >> 32), static_cast<uint32_t>(b),
+           static_cast<uint32_t>(b >> 32), static_cast<uint32_t>(c),
+           static_cast<uint32_t>(c >> 32)};
+  if ((s.v | s.w | s.x | s.y | s.z) == 0) s.v = 1;
+  for (int i = 0; i < 64; ++i) xorwow_step(s);
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// Box-Muller (stream.hpp:57-62): r = sqrt(-2 log u1), a = 2 pi u2,
+// (r cos a, r sin a); u1 <= 0 clamps to 2^-64. sqrt and the products are
+// correctly rounded like glibc's; log/sin/cos are CUDA's (<= 1-2 ulp), the
+// one documented non-bit-identical step (normals-in mode is exact).
+// ---------------------------------------------------------------------------
+constexpr double kTwoPi = 6.283185307179586;  // 2.0 * std::numbers::pi, exact doubling
+
+__device__ __forceinline__ void box_muller(double u1, double u2, double& z1, double& z2) {
+  if (u1 <= 0.0) u1 = 0x1p-64;
+  const double r = __dsqrt_rn(__dmul_rn(-2.0, log(u1)));
+  const double a = __dmul_rn(kTwoPi, u2);
+  double s, c;
+  sincos(a, &s, &c);
+  z1 = __dmul_rn(r, c);
+  z2 = __dmul_rn(r, s);
+}
+
+// ---------------------------------------------------------------------------
+// Normal sources: one per engine plus the parity-mode reader. Each models a
+// PathStreamer positioned at a path (or Alg III sample) and hands out that
+// unit's normals in order, Box-Muller mate cached (stream.hpp:97-108) and
+// dropped at the unit boundary.
+// ---------------------------------------------------------------------------
+enum : int { kSrcLcg48 = 0, kSrcMrg = 1, kSrcXorwow = 2, kSrcNormalsIn = 3 };
+
+// SrcArgs (engine seeds, jump tables, parity-mode normals) lives in qt_internal.h.
+
+
+template <int SRC>
+struct Source;
+
+template <>
+struct Source<kSrcMrg> {
+  Mrg s;
+  double spare;
+  bool has;
+  // Position at the first draw of `unit` (unit * draws serial draws in).
+  __device__ __forceinline__ void start(const SrcArgs& a, uint64_t unit) {
+    s = Mrg{a.mrg_seed[0], a.mrg_seed[1], a.mrg_seed[2], a.mrg_seed[3], a.mrg_seed[4], a.mrg_seed[5]};
+    mrg_jump(s, unit * a.draws, a.mrg_table);
+    has = false;
+  }
+  // Units are contiguous blocks of the serial stream, so after a unit has
+  // consumed its `draws` uniforms the state already sits on the next unit.
+  __device__ __forceinline__ void next_unit(const SrcArgs&, uint64_t) { has = false; }
+  __device__ __forceinline__ double uniform() { return mrg_to_unit(mrg_step(s)); }
+  __device__ __forceinline__ double normal() {
+    if (has) {
+      has = false;
+      return spare;
+    }
+    const double u1 = uniform();
+    const double u2 = uniform();
+    double z1;
+    box_muller(u1, u2, z1, spare);
+    has = true;
+    return z1;
+  }
+};
+
+template <>
+struct Source<kSrcLcg48> {
+  uint64_t x;
+  double spare;
+  bool has;
+  __device__ __forceinline__ void start(const SrcArgs& a, uint64_t unit) {
+    x = a.lcg_seed;
+    lcg_jump(x, unit * a.draws, a.lcg_table);
+    has = false;
+  }
+  __device__ __forceinline__ void next_unit(const SrcArgs&, uint64_t) { has = false; }
+  __device__ __forceinline__ double uniform() { return lcg_uniform(x); }
+  __device__ __forceinline__ double normal() {
+    if (has) {
+      has = false;
+      return spare;
+    }
+    const double u1 = uniform();
+    const double u2 = uniform();
+    double z1;
+    box_muller(u1, u2, z1, spare);
+    has = true;
+    return z1;
+  }
+};
+
+template <>
+struct Source<kSrcXorwow> {
+  Xorwow s;
+  double spare;
+  bool has;
+  __device__ __forceinline__ void start(const SrcArgs& a, uint64_t unit) {
+    s = xorwow_stream(a.seed, unit);
+    has = false;
+  }
+  __device__ __forceinline__ void next_unit(const SrcArgs& a, uint64_t unit) { start(a, unit); }
+  __device__ __forceinline__ double uniform() {
+    return __uint2double_rn(xorwow_step(s)) * 0x1p-32;
+  }
+  __device__ __forceinline__ double normal() {
+    if (has) {
+      has = false;
+      return spare;
+    }
+    const double u1 = uniform();
+    const double u2 = uniform();
+    double z1;
+    box_muller(u1, u2, z1, spare);
+    has = true;
+    return z1;
+  }
+};
+
+template <>
+struct Source<kSrcNormalsIn> {
+  const double* p;
+  __device__ __forceinline__ void start(const SrcArgs& a, uint64_t unit) {
+    p = a.normals + (unit - a.normals_first) * a.per_unit;
+  }
+  __device__ __forceinline__ void next_unit(const SrcArgs& a, uint64_t unit) { start(a, unit); }
+  __device__ __forceinline__ double normal() { return __ldg(p++); }
+};
+
+// ---------------------------------------------------------------------------
+// Chains (model/chains.hpp). K = qt_chain_kind.
+// ---------------------------------------------------------------------------
+template <int K>
+struct Chain;
+
+template <>
+struct Chain<0> {  // BrownianChain1d: x + sqrt(dt) eps (chains.hpp:83-86)
+  static constexpr int D = 1, NPS = 1;
+  __device__ __forceinline__ static void step(const double* c, const double* x, double* o,
+                                              const double* e) {
+    o[0] = __dadd_rn(x[0], __dmul_rn(c[0], e[0]));
+  }
+  __device__ __forceinline__ static void marginal(const double* m, bool origin, double* o,
+                                                  const double* e) {
+    o[0] = origin ? 0.0 : __dmul_rn(m[0], e[0]);  // k == 0 -> exactly 0 (chains.hpp:89)
+  }
+};
+
+template <>
+struct Chain<1> {  // TwoFactorChain (chains.hpp:48-59)
+  static constexpr int D = 2, NPS = 2;
+  __device__ __forceinline__ static void step(const double* c, const double* x, double* o,
+                                              const double* e) {
+    o[0] = __dadd_rn(__dmul_rn(c[0], x[0]), __dmul_rn(c[2], e[0]));
+    o[1] = __dadd_rn(__dadd_rn(__dmul_rn(c[1], x[1]), __dmul_rn(c[3], e[0])),
+                     __dmul_rn(c[4], e[1]));
+  }
+  __device__ __forceinline__ static void marginal(const double* m, bool, double* o,
+                                                  const double* e) {
+    o[0] = __dmul_rn(m[0], e[0]);
+    o[1] = __dadd_rn(__dmul_rn(m[1], e[0]), __dmul_rn(m[2], e[1]));
+  }
+};
+
+template <>
+struct Chain<2> {  // OU 1-D = factor 1 of TwoFactorChain
+  static constexpr int D = 1, NPS = 1;
+  __device__ __forceinline__ static void step(const double* c, const double* x, double* o,
+                                              const double* e) {
+    o[0] = __dadd_rn(__dmul_rn(c[0], x[0]), __dmul_rn(c[2], e[0]));
+  }
+  __device__ __forceinline__ static void marginal(const double* m, bool, double* o,
+                                                  const double* e) {
+    o[0] = __dmul_rn(m[0], e[0]);
+  }
+};
+
+template <>
+struct Chain<3> {  // GBM 3-D basket log-state
+  static constexpr int D = 3, NPS = 3;
+  __device__ __forceinline__ static void step(const double* c, const double* x, double* o,
+                                              const double* e) {
+    o[0] = __dadd_rn(x[0], __dmul_rn(c[0], e[0]));
+    o[1] = __dadd_rn(x[1], __dadd_rn(__dmul_rn(c[1], e[0]), __dmul_rn(c[2], e[1])));
+    o[2] = __dadd_rn(x[2], __dadd_rn(__dadd_rn(__dmul_rn(c[3], e[0]), __dmul_rn(c[4], e[1])),
+                                     __dmul_rn(c[5], e[2])));
+  }
+  __device__ __forceinline__ static void marginal(const double* m, bool, double* o,
+                                                  const double* e) {
+    o[0] = __dmul_rn(m[0], e[0]);
+    o[1] = __dadd_rn(__dmul_rn(m[1], e[0]), __dmul_rn(m[2], e[1]));
+    o[2] = __dadd_rn(__dadd_rn(__dmul_rn(m[3], e[0]), __dmul_rn(m[4], e[1])),
+                     __dmul_rn(m[5], e[2]));
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Voronoi projection (nearest_brute, nn.hpp:18-46): exact argmin of the
+// reference's d2, smallest original index on ties.
+// ---------------------------------------------------------------------------
+
+// Exact scan over the sorted records with (d2, original index) ordering:
+// identical result to the reference's ascending strict-< scan for every x.
+__device__ __noinline__ uint32_t nearest_1d_scan(const Rec1* R, uint32_t n, double x) {
+  uint32_t best = 0;
+  double bd = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  for (uint32_t s = 1; s <= n; ++s) {
+    const double d = __dsub_rn(x, R[s].v);
+    const double d2 = __dmul_rn(d, d);
+    if (d2 < bd || (d2 == bd && R[s].orig < best)) {
+      bd = d2;
+      best = R[s].orig;
+    }
+  }
+  return best;
+}
+
+// d == 1: bucket jump into the sorted records, bracket, compare the two
+// neighbours. Exact whenever |x| < x_safe (no same-side ties possible, see
+// DESIGN.md "1-D projection"); otherwise (or for NaN/inf) the exact scan.
+__device__ __forceinline__ uint32_t nearest_1d(const LayerTable& h, const uint8_t* base, double x) {
+  const Rec1* R = reinterpret_cast<const Rec1*>(base + h.off_rec);
+  if (!(fabs(x) < h.x_safe)) return nearest_1d_scan(R, h.n_pts, x);
+  const uint16_t* start = reinterpret_cast<const uint16_t*>(base + h.off_start);
+  const uint32_t b = bucket_of(x, h.lo, h.inv_w, h.nb_d, h.nb);
+  uint32_t s = start[b];  // R[s] = sorted point s-1 < x (or -inf sentinel)
+  Rec1 lo = R[s], hi = R[s + 1];
+  if (!(x < hi.v)) {
+    lo = hi;
+    hi = R[s + 2];
+    if (!(x < hi.v)) {
+      s += 2;
+      while (!(x < R[s + 1].v)) ++s;
+      lo = R[s];
+      hi = R[s + 1];
+    }
+  }
+  const double dl = __dsub_rn(x, lo.v);
+  const double dh = __dsub_rn(x, hi.v);
+  const double d2l = __dmul_rn(dl, dl);
+  const double d2h = __dmul_rn(dh, dh);
+  return d2l < d2h ? lo.orig : (d2h < d2l ? hi.orig : min(lo.orig, hi.orig));
+}
+
+// d == 2: the reference's fast path dx*dx + dy*dy (nn.hpp:25-37), strict <.
+__device__ __forceinline__ uint32_t nearest_2d(const LayerTable& h, const uint8_t* base,
+                                               const double* q) {
+  const double2* P = reinterpret_cast<const double2*>(base + h.off_rec);
+  uint32_t best = 0;
+  double bd = __longlong_as_double(0x7ff0000000000000ll);
+  const uint32_t n = h.n_pts;
+  for (uint32_t i = 0; i < n; ++i) {
+    const double2 p = P[i];
+    const double dx = __dsub_rn(q[0], p.x);
+    const double dy = __dsub_rn(q[1], p.y);
+    const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+    if (d2 < bd) {
+      bd = d2;
+      best = i;
+    }
+  }
+  return best;
+}
+
+// d == 3: squared_distance accumulated from 0.0 in coordinate order
+// (grid.hpp:65-72), strict < (nn.hpp:38-45).
+__device__ __forceinline__ uint32_t nearest_3d(const LayerTable& h, const uint8_t* base,
+                                               const double* q) {
+  const double* P = reinterpret_cast<const double*>(base + h.off_rec);
+  uint32_t best = 0;
+  double bd = __longlong_as_double(0x7ff0000000000000ll);
+  const uint32_t n = h.n_pts;
+  for (uint32_t i = 0; i < n; ++i) {
+    const double d0 = __dsub_rn(q[0], P[3 * i]);
+    const double d1 = __dsub_rn(q[1], P[3 * i + 1]);
+    const double d2_ = __dsub_rn(q[2], P[3 * i + 2]);
+    double acc = __dadd_rn(0.0, __dmul_rn(d0, d0));
+    acc = __dadd_rn(acc, __dmul_rn(d1, d1));
+    acc = __dadd_rn(acc, __dmul_rn(d2_, d2_));
+    if (acc < bd) {
+      bd = acc;
+      best = i;
+    }
+  }
+  return best;
+}
+
+template <int D>
+__device__ __forceinline__ uint32_t nearest(const LayerTable& h, const uint8_t* base,
+                                            const double* q) {
+  if constexpr (D == 1) return nearest_1d(h, base, q[0]);
+  else if constexpr (D == 2) return nearest_2d(h, base, q);
+  else return nearest_3d(h, base, q);
+}
+
+// ---------------------------------------------------------------------------
+// Async bulk copy global -> shared with mbarrier completion (TMA bulk path,
+// SASS UBLKCP), and the mbarrier primitives.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// bytes must be a multiple of 16, both addresses 16-byte aligned.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// No-return 64-bit atomic add (SASS RED.E.ADD.64): the count tally
+// `joint[t][i*N_k+j] += 1` (estimate.hpp:118).
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+}  // namespace qt

@@ -1,0 +1,79 @@
+// qt_internal.h -- kernel argument blocks and launchers shared by
+// qt_kernels.cu (device) and qt_capi.cu (host runtime).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "qt_layout.h"
+
+namespace qt {
+
+// Normal-source parameters (see Source<> in qt_device.cuh).
+struct SrcArgs {
+  uint32_t mrg_seed[6];
+  uint64_t lcg_seed;
+  uint64_t seed;
+  const uint32_t* mrg_table;
+  const unsigned long long* lcg_table;
+  const double* normals;
+  uint64_t normals_first;
+  uint64_t draws;
+  uint32_t per_unit;
+};
+
+struct PathArgs {
+  SrcArgs src;
+  const uint8_t* tables;      // layer tables, concatenated, 16-byte aligned
+  const uint32_t* tab_off;    // [n] byte offset of layer k's table (index k-1)
+  const uint32_t* tab_bytes;  // [n]
+  unsigned long long* joint;
+  uint64_t first;             // first path of the window
+  uint64_t q, rem;            // window split over T threads: q each, +1 for the first rem
+  uint32_t n;
+  uint32_t buf_bytes;         // staging buffer size (max table bytes)
+  uint32_t resident_bytes;    // sum of table bytes (resident mode)
+};
+
+struct Alg3Args {
+  SrcArgs src;
+  const uint8_t* tables;
+  const uint32_t* tab_off;
+  const uint32_t* tab_bytes;
+  unsigned long long* joint;
+  uint64_t M;             // samples per layer
+  uint64_t first, count;  // unit window within [0, n M)
+  uint32_t n;
+  uint32_t buf_bytes;
+};
+
+struct FinalizeArgs {
+  const uint64_t* rows;      // [n] N_{t}
+  const uint64_t* cols;      // [n] N_{t+1}
+  const uint64_t* joff;      // [n] joint offset of transition t
+  const uint64_t* voff_row;  // [n] visits offset of layer t
+  const uint64_t* voff_col;  // [n] visits offset of layer t+1
+};
+
+// shared error text / launch counter (defined in qt_capi.cu)
+void note_error(const std::string& msg);
+void note_launches(uint64_t n);
+
+cudaError_t launch_paths(int kind, int src, bool resident, const PathArgs& a, uint32_t blocks,
+                         size_t smem, cudaStream_t st);
+int paths_blocks_per_sm(int kind, int src, bool resident, size_t smem);
+cudaError_t launch_alg3(int kind, int src, const Alg3Args& a, uint32_t slices, size_t smem,
+                        cudaStream_t st);
+cudaError_t launch_finalize(bool alg3, const unsigned long long* joint, unsigned long long* visits,
+                            double* pi, uint64_t samples, const FinalizeArgs& f, uint32_t n,
+                            uint64_t max_cols, uint64_t max_rows, uint64_t max_elems,
+                            cudaStream_t st, int* launches);
+cudaError_t launch_nearest(int dim, const uint8_t* table, uint32_t bytes, const double* q,
+                           uint64_t nq, unsigned long long* out, cudaStream_t st);
+cudaError_t launch_path_normals(int src, const SrcArgs& a, uint64_t first, uint64_t count,
+                                double* out, cudaStream_t st);
+cudaError_t launch_uniforms(int src, const SrcArgs& a, uint64_t offset, uint64_t count,
+                            double* out, cudaStream_t st);
+
+}  // namespace qt

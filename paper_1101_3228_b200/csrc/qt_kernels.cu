@@ -1,0 +1,455 @@
+// qt_kernels.cu -- the sm_100a kernels of the transition estimator.
+//
+//  k_paths   K1+K2+K3 fused: Alg I/II path kernel (estimate.hpp:88-126). One
+//            thread owns a contiguous run of paths (so its MRG32k3a state
+//            flows from path to path without jumps), the CTA walks the layers
+//            in lock-step and double-buffers each layer's grid table into
+//            shared memory with cp.async.bulk + mbarrier; each transition is
+//            normals -> chain step -> exact Voronoi projection -> one
+//            red.global.add.u64 into joint[k-1][i*N_k + j].
+//  k_alg3    K4: Alg III layer-parallel pair sampler (estimate.hpp:213-265):
+//            CTA = (layer k, slice of its M samples), tables of layers k-1 and
+//            k resident in shared memory, two projections per sample.
+//  k_colsum / k_rowsum / k_normalize
+//            visits from the joint counts + row normalisation (quant_tree.hpp:69-83).
+//  k_nearest, k_path_normals, k_uniforms  standalone K2 and RNG probes.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qt_device.cuh"
+#include "qt_internal.h"
+
+namespace qt {
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// Alg I / II
+// ---------------------------------------------------------------------------
+template <int K, int SRC, bool RESIDENT>
+__global__ void __launch_bounds__(kThreads) k_paths(const PathArgs a) {
+  using C = Chain<K>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bars[2];
+  const uint32_t tid = threadIdx.x;
+  const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + tid;
+  const uint64_t mycount = a.q + (g < a.rem ? 1u : 0u);
+  const uint64_t mybeg = a.first + g * a.q + (g < a.rem ? g : a.rem);
+  const uint64_t rounds = a.q + (a.rem ? 1u : 0u);
+  const uint64_t steps_total = rounds * a.n;
+  if (steps_total == 0) return;
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if constexpr (RESIDENT) {
+    // Every layer table fits: stage them all once, no per-layer barrier.
+    if (tid == 0) {
+      mbar_expect_tx(&bars[0], a.resident_bytes);
+      for (uint32_t k = 0; k < a.n; ++k)
+        bulk_g2s(smem + (a.tab_off[k] - a.tab_off[0]), a.tables + a.tab_off[k], a.tab_bytes[k],
+                 &bars[0]);
+    }
+    mbar_wait(&bars[0], 0);
+  } else {
+    if (tid == 0) {
+      for (uint32_t s = 0; s < 2 && s < steps_total; ++s) {
+        const uint32_t k = static_cast<uint32_t>(s % a.n);
+        mbar_expect_tx(&bars[s], a.tab_bytes[k]);
+        bulk_g2s(smem + s * a.buf_bytes, a.tables + a.tab_off[k], a.tab_bytes[k], &bars[s]);
+      }
+    }
+  }
+
+  Source<SRC> src;
+  if (mycount) src.start(a.src, mybeg);
+  uint64_t step_no = 0;
+  for (uint64_t r = 0; r < rounds; ++r) {
+    const bool active = r < mycount;
+    if (active && r > 0) src.next_unit(a.src, mybeg + r);
+    double x[C::D];
+#pragma unroll
+    for (int d = 0; d < C::D; ++d) x[d] = 0.0;  // initial(): the origin (chains.hpp:43-46,81)
+    uint32_t i = 0;                             // layer 0 is the singleton {x0}
+    for (uint32_t k = 1; k <= a.n; ++k, ++step_no) {
+      const uint8_t* tb;
+      if constexpr (RESIDENT) {
+        tb = smem + (a.tab_off[k - 1] - a.tab_off[0]);
+      } else {
+        const uint32_t b = static_cast<uint32_t>(step_no & 1u);
+        tb = smem + b * a.buf_bytes;
+        mbar_wait(&bars[b], static_cast<uint32_t>((step_no >> 1) & 1u));
+      }
+      const LayerTable& h = *reinterpret_cast<const LayerTable*>(tb);
+      if (active) {
+        double e[C::NPS], xn[C::D];
+#pragma unroll
+        for (int q = 0; q < C::NPS; ++q) e[q] = src.normal();
+        C::step(h.step, x, xn, e);
+#pragma unroll
+        for (int d = 0; d < C::D; ++d) x[d] = xn[d];
+        const uint32_t j = nearest<C::D>(h, tb, x);
+        red_add_u64(a.joint + h.joff + static_cast<uint64_t>(i) * h.n_pts + j, 1ull);
+        i = j;
+      }
+      if constexpr (!RESIDENT) {
+        __syncthreads();  // every thread is done with this buffer
+        if (tid == 0) {
+          const uint64_t s2 = step_no + 2;
+          if (s2 < steps_total) {
+            const uint32_t b = static_cast<uint32_t>(step_no & 1u);
+            const uint32_t kk = static_cast<uint32_t>(s2 % a.n);
+            mbar_expect_tx(&bars[b], a.tab_bytes[kk]);
+            bulk_g2s(smem + b * a.buf_bytes, a.tables + a.tab_off[kk], a.tab_bytes[kk], &bars[b]);
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Alg III: grid = (slices, n). Slice s of layer k covers samples
+// [M s / S, M (s+1) / S) of that layer; each thread a contiguous sub-run, so
+// its stream again flows sample to sample without jumps.
+// ---------------------------------------------------------------------------
+template <int K, int SRC>
+__global__ void __launch_bounds__(kThreads) k_alg3(const Alg3Args a) {
+  using C = Chain<K>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t k = blockIdx.y + 1;  // transition k-1 -> k
+  const uint64_t layer0 = static_cast<uint64_t>(k - 1) * a.M;
+  // slice of this layer, intersected with the unit window [first, first+count)
+  uint64_t lo = layer0 + a.M * blockIdx.x / gridDim.x;
+  uint64_t hi = layer0 + a.M * (blockIdx.x + 1) / gridDim.x;
+  lo = lo > a.first ? lo : a.first;
+  hi = hi < a.first + a.count ? hi : a.first + a.count;
+  if (lo >= hi) return;
+  const uint64_t len = hi - lo;
+  const uint64_t q = len / blockDim.x, rem = len % blockDim.x;
+  const uint64_t mycount = q + (tid < rem ? 1u : 0u);
+  const uint64_t mybeg = lo + tid * q + (tid < rem ? tid : rem);
+
+  // tables: layer k at buffer 0, layer k-1 (k >= 2) at buffer 1
+  const uint8_t* tk = smem;
+  const uint8_t* tp = smem + a.buf_bytes;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    const uint32_t bytes = a.tab_bytes[k - 1] + (k >= 2 ? a.tab_bytes[k - 2] : 0u);
+    mbar_expect_tx(&bar, bytes);
+    bulk_g2s(smem, a.tables + a.tab_off[k - 1], a.tab_bytes[k - 1], &bar);
+    if (k >= 2) bulk_g2s(smem + a.buf_bytes, a.tables + a.tab_off[k - 2], a.tab_bytes[k - 2], &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const LayerTable& hk = *reinterpret_cast<const LayerTable*>(tk);
+  const LayerTable& hp = *reinterpret_cast<const LayerTable*>(tp);
+
+  Source<SRC> src;
+  if (mycount) src.start(a.src, mybeg);
+  for (uint64_t r = 0; r < mycount; ++r) {
+    if (r > 0) src.next_unit(a.src, mybeg + r);
+    double e[C::D + C::NPS], x[C::D], xn[C::D];
+#pragma unroll
+    for (int q2 = 0; q2 < C::D + C::NPS; ++q2) e[q2] = src.normal();
+    C::marginal(hk.marg_prev, k == 1, x, e);  // sample_marginal(k-1, ...)
+    C::step(hk.step, x, xn, e + C::D);        // step(k-1, ...)
+    const uint32_t i = k == 1 ? 0u : nearest<C::D>(hp, tp, x);
+    const uint32_t j = nearest<C::D>(hk, tk, xn);
+    red_add_u64(a.joint + hk.joff + static_cast<uint64_t>(i) * hk.n_pts + j, 1ull);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// finalize
+// ---------------------------------------------------------------------------
+// visits[k][j] = sum_i joint[k-1][i][j]  (grid.y = transition t = k-1)
+__global__ void k_colsum(const unsigned long long* joint, unsigned long long* visits,
+                         const FinalizeArgs a) {
+  const uint32_t t = blockIdx.y;
+  const uint64_t rows = a.rows[t], cols = a.cols[t];
+  const unsigned long long* J = joint + a.joff[t];
+  unsigned long long* V = visits + a.voff_col[t];
+  for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < cols;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    unsigned long long s = 0;
+    for (uint64_t i = 0; i < rows; ++i) s += J[i * cols + j];
+    V[j] = s;
+  }
+}
+
+// visits[t][i] = sum_j joint[t][i][j]: one warp per row  (Alg III sources)
+__global__ void k_rowsum(const unsigned long long* joint, unsigned long long* visits,
+                         const FinalizeArgs a) {
+  const uint32_t t = blockIdx.y;
+  const uint64_t rows = a.rows[t], cols = a.cols[t];
+  const unsigned long long* J = joint + a.joff[t];
+  unsigned long long* V = visits + a.voff_row[t];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < rows;
+       i += warps) {
+    unsigned long long s = 0;
+    for (uint64_t j = lane; j < cols; j += 32) s += J[i * cols + j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) V[i] = s;
+  }
+}
+
+// pi[t][i][j] = joint / visits[t][i] (0 on unvisited rows), quant_tree.hpp:69-83
+__global__ void k_normalize(const unsigned long long* joint, const unsigned long long* visits,
+                            double* pi, const FinalizeArgs a) {
+  const uint32_t t = blockIdx.y;
+  const uint64_t cols = a.cols[t];
+  const uint64_t total = a.rows[t] * cols;
+  const unsigned long long* J = joint + a.joff[t];
+  const unsigned long long* V = visits + a.voff_row[t];
+  double* P = pi + a.joff[t];
+  for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long den = V[e / cols];
+    P[e] = den == 0 ? 0.0 : __ddiv_rn(__ull2double_rn(J[e]), __ull2double_rn(den));
+  }
+}
+
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+
+// ---------------------------------------------------------------------------
+// standalone K2 (NnIndex::nearest in batch) and RNG probes
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_nearest(const uint8_t* table, uint32_t bytes,
+                                                      const double* queries, uint64_t nq,
+                                                      unsigned long long* out, int in_smem) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar;
+  const uint8_t* tb = table;
+  if (in_smem) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+      mbar_expect_tx(&bar, bytes);
+      bulk_g2s(smem, table, bytes, &bar);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    tb = smem;
+  }
+  const LayerTable& h = *reinterpret_cast<const LayerTable*>(tb);
+  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < nq;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    double x[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) x[d] = queries[q * D + d];
+    out[q] = nearest<D>(h, tb, x);
+  }
+}
+
+template <int SRC>
+__global__ void k_path_normals(const SrcArgs a, uint64_t first, uint64_t count, double* out) {
+  const uint64_t u = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u >= count) return;
+  Source<SRC> src;
+  src.start(a, first + u);
+  for (uint32_t e = 0; e < a.per_unit; ++e) out[u * a.per_unit + e] = src.normal();
+}
+
+template <int SRC>
+__global__ void k_uniforms(const SrcArgs a, uint64_t offset, uint64_t count, double* out) {
+  const uint64_t u = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u >= count) return;
+  SrcArgs b = a;
+  b.draws = 1;  // position at serial draw offset + u
+  Source<SRC> src;
+  src.start(b, offset + u);
+  out[u] = src.uniform();
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+template <int K, int SRC, bool RES>
+static cudaError_t launch_paths_t(const PathArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
+  auto fn = k_paths<K, SRC, RES>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  fn<<<grid, kThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int K, int SRC>
+static cudaError_t launch_paths_r(const PathArgs& a, bool res, dim3 g, size_t smem,
+                                  cudaStream_t st) {
+  return res ? launch_paths_t<K, SRC, true>(a, g, smem, st)
+             : launch_paths_t<K, SRC, false>(a, g, smem, st);
+}
+
+template <int K>
+static cudaError_t launch_paths_s(const PathArgs& a, int src, bool res, dim3 g, size_t smem,
+                                  cudaStream_t st) {
+  switch (src) {
+    case kSrcLcg48: return launch_paths_r<K, kSrcLcg48>(a, res, g, smem, st);
+    case kSrcMrg: return launch_paths_r<K, kSrcMrg>(a, res, g, smem, st);
+    case kSrcXorwow: return launch_paths_r<K, kSrcXorwow>(a, res, g, smem, st);
+    default: return launch_paths_r<K, kSrcNormalsIn>(a, res, g, smem, st);
+  }
+}
+
+cudaError_t launch_paths(int kind, int src, bool resident, const PathArgs& a, uint32_t blocks,
+                         size_t smem, cudaStream_t st) {
+  const dim3 g(blocks);
+  switch (kind) {
+    case 0: return launch_paths_s<0>(a, src, resident, g, smem, st);
+    case 1: return launch_paths_s<1>(a, src, resident, g, smem, st);
+    case 2: return launch_paths_s<2>(a, src, resident, g, smem, st);
+    default: return launch_paths_s<3>(a, src, resident, g, smem, st);
+  }
+}
+
+int paths_blocks_per_sm(int kind, int src, bool resident, size_t smem) {
+  const void* fn = nullptr;
+#define QT_PICK(K, S)                                                                   \
+  fn = resident ? reinterpret_cast<const void*>(k_paths<K, S, true>)                   \
+                : reinterpret_cast<const void*>(k_paths<K, S, false>)
+#define QT_PICK_S(K)                      \
+  switch (src) {                          \
+    case kSrcLcg48: QT_PICK(K, kSrcLcg48); break; \
+    case kSrcMrg: QT_PICK(K, kSrcMrg); break;     \
+    case kSrcXorwow: QT_PICK(K, kSrcXorwow); break; \
+    default: QT_PICK(K, kSrcNormalsIn); break;    \
+  }
+  switch (kind) {
+    case 0: QT_PICK_S(0); break;
+    case 1: QT_PICK_S(1); break;
+    case 2: QT_PICK_S(2); break;
+    default: QT_PICK_S(3); break;
+  }
+#undef QT_PICK_S
+#undef QT_PICK
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem) != cudaSuccess)
+    return 1;
+  return nb > 0 ? nb : 1;
+}
+
+template <int K, int SRC>
+static cudaError_t launch_alg3_t(const Alg3Args& a, dim3 grid, size_t smem, cudaStream_t st) {
+  auto fn = k_alg3<K, SRC>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  fn<<<grid, kThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int K>
+static cudaError_t launch_alg3_s(const Alg3Args& a, int src, dim3 g, size_t smem,
+                                 cudaStream_t st) {
+  switch (src) {
+    case kSrcLcg48: return launch_alg3_t<K, kSrcLcg48>(a, g, smem, st);
+    case kSrcMrg: return launch_alg3_t<K, kSrcMrg>(a, g, smem, st);
+    case kSrcXorwow: return launch_alg3_t<K, kSrcXorwow>(a, g, smem, st);
+    default: return launch_alg3_t<K, kSrcNormalsIn>(a, g, smem, st);
+  }
+}
+
+cudaError_t launch_alg3(int kind, int src, const Alg3Args& a, uint32_t slices, size_t smem,
+                        cudaStream_t st) {
+  const dim3 g(slices, a.n);
+  switch (kind) {
+    case 0: return launch_alg3_s<0>(a, src, g, smem, st);
+    case 1: return launch_alg3_s<1>(a, src, g, smem, st);
+    case 2: return launch_alg3_s<2>(a, src, g, smem, st);
+    default: return launch_alg3_s<3>(a, src, g, smem, st);
+  }
+}
+
+cudaError_t launch_finalize(bool alg3, const unsigned long long* joint, unsigned long long* visits,
+                            double* pi, uint64_t samples, const FinalizeArgs& f, uint32_t n,
+                            uint64_t max_cols, uint64_t max_rows, uint64_t max_elems,
+                            cudaStream_t st, int* launches) {
+  int l = 0;
+  const uint32_t bx_cols = static_cast<uint32_t>((max_cols + 255) / 256);
+  if (!alg3) {
+    // visits[0][0] = M, visits[k] = column sums of joint[k-1]
+    k_set_u64<<<1, 1, 0, st>>>(visits, samples);
+    ++l;
+    k_colsum<<<dim3(bx_cols, n), 256, 0, st>>>(joint, visits, f);
+    ++l;
+  } else {
+    // visits[k-1] = row sums of joint[k-1] (sources), visits[n] = col sums of joint[n-1]
+    const uint32_t bx_rows = static_cast<uint32_t>((max_rows * 32 + 255) / 256);
+    k_rowsum<<<dim3(bx_rows < 4096 ? bx_rows : 4096, n), 256, 0, st>>>(joint, visits, f);
+    ++l;
+    FinalizeArgs last = f;
+    last.rows += n - 1;
+    last.cols += n - 1;
+    last.joff += n - 1;
+    last.voff_col += n - 1;
+    k_colsum<<<dim3(bx_cols, 1), 256, 0, st>>>(joint, visits, last);
+    ++l;
+  }
+  const uint64_t want = (max_elems + 255) / 256;
+  const uint32_t bx = static_cast<uint32_t>(want < 2048 ? want : 2048);
+  k_normalize<<<dim3(bx, n), 256, 0, st>>>(joint, visits, pi, f);
+  ++l;
+  if (launches) *launches += l;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nearest(int dim, const uint8_t* table, uint32_t bytes, const double* q,
+                           uint64_t nq, unsigned long long* out, cudaStream_t st) {
+  const bool in_smem = bytes <= 200u * 1024u;
+  const size_t smem = in_smem ? bytes : 0;
+  uint64_t want = (nq + kThreads - 1) / kThreads;
+  const uint32_t blocks = static_cast<uint32_t>(want < 148u * 16u ? (want ? want : 1) : 148u * 16u);
+  cudaError_t e;
+  switch (dim) {
+    case 1:
+      cudaFuncSetAttribute(k_nearest<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_nearest<1><<<blocks, kThreads, smem, st>>>(table, bytes, q, nq, out, in_smem);
+      break;
+    case 2:
+      cudaFuncSetAttribute(k_nearest<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_nearest<2><<<blocks, kThreads, smem, st>>>(table, bytes, q, nq, out, in_smem);
+      break;
+    default:
+      cudaFuncSetAttribute(k_nearest<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_nearest<3><<<blocks, kThreads, smem, st>>>(table, bytes, q, nq, out, in_smem);
+  }
+  e = cudaGetLastError();
+  return e;
+}
+
+cudaError_t launch_path_normals(int src, const SrcArgs& a, uint64_t first, uint64_t count,
+                                double* out, cudaStream_t st) {
+  const uint32_t blocks = static_cast<uint32_t>((count + 127) / 128);
+  switch (src) {
+    case kSrcLcg48: k_path_normals<kSrcLcg48><<<blocks, 128, 0, st>>>(a, first, count, out); break;
+    case kSrcMrg: k_path_normals<kSrcMrg><<<blocks, 128, 0, st>>>(a, first, count, out); break;
+    default: k_path_normals<kSrcXorwow><<<blocks, 128, 0, st>>>(a, first, count, out);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_uniforms(int src, const SrcArgs& a, uint64_t offset, uint64_t count,
+                            double* out, cudaStream_t st) {
+  const uint32_t blocks = static_cast<uint32_t>((count + 127) / 128);
+  if (src == kSrcLcg48)
+    k_uniforms<kSrcLcg48><<<blocks, 128, 0, st>>>(a, offset, count, out);
+  else
+    k_uniforms<kSrcMrg><<<blocks, 128, 0, st>>>(a, offset, count, out);
+  return cudaGetLastError();
+}
+
+}  // namespace qt

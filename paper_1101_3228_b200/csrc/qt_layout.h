@@ -1,0 +1,67 @@
+// qt_layout.h -- host/device shared layout of the per-layer "grid tables"
+// that the path kernels stage into shared memory with cp.async.bulk.
+//
+// One table per layer k = 1..n, 16-byte aligned, contiguous in HBM:
+//
+//   LayerTable header (192 B)
+//   d == 1 : Rec1[N + 2]       sorted points {value, original index}, with
+//                              -inf / +inf sentinels at [0] and [N + 1]
+//            uint16 start[nb]  bucket -> first sorted position whose bucket >= b
+//   d >= 2 : double pts[N * d] points in ORIGINAL order (row-major), the
+//                              reference's scan order (nn.hpp:25-45)
+//
+// The header also carries the chain coefficients of the transition that lands
+// on this layer (step of k-1 -> k) and the marginal factor of layer k-1, so a
+// CTA that holds a layer's table in shared memory has everything one step needs.
+#pragma once
+#include <stdint.h>
+
+namespace qt {
+
+struct alignas(16) LayerTable {
+  double lo;            // d == 1: smallest grid value (bucket origin)
+  double inv_w;         // d == 1: buckets per unit of x
+  double x_safe;        // d == 1: |x| < x_safe => no same-side d2 ties (fast path exact)
+  double nb_d;          // (double)nb
+  double step[6];       // chain coefficients of transition k-1 -> k
+  double marg_prev[6];  // marginal factor of layer k-1 (Alg III)
+  uint64_t joff;        // element offset of joint[k-1] in the flat joint array
+  uint64_t voff;        // element offset of visits[k]
+  uint32_t n_pts;       // N_k
+  uint32_t n_prev;      // N_{k-1}
+  uint32_t nb;          // d == 1: number of buckets
+  uint32_t off_rec;     // byte offset of Rec1[] / pts[] from the table start
+  uint32_t off_start;   // byte offset of start[] (d == 1)
+  uint32_t bytes;       // total table bytes (multiple of 16)
+  uint32_t layer;       // k
+  uint32_t dim;
+  uint32_t pad_[4];
+};
+static_assert(sizeof(LayerTable) == 192, "LayerTable header is 192 bytes");
+
+struct alignas(16) Rec1 {
+  double v;
+  uint32_t orig;
+  uint32_t pad;
+};
+static_assert(sizeof(Rec1) == 16, "Rec1 is 16 bytes");
+
+constexpr uint32_t kNoIndex = 0xFFFFFFFFu;
+
+// Bucket of x under a layer's (lo, inv_w, nb): identical IEEE operations on
+// host and device (one subtraction, one multiplication, truncation), so the
+// start[] table built on the host is exact for every device query.
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline uint32_t bucket_of(double x, double lo, double inv_w, double nb_d, uint32_t nb) {
+#if defined(__CUDA_ARCH__)
+  const double t = __dmul_rn(__dsub_rn(x, lo), inv_w);
+#else
+  volatile double d = x - lo;  // volatile: no contraction or reassociation
+  const double t = d * inv_w;
+#endif
+  return t > 0.0 ? (t < nb_d ? static_cast<uint32_t>(t) : nb - 1u) : 0u;
+}
+
+}  // namespace qt

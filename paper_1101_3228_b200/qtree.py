@@ -1,0 +1,549 @@
+"""Python mirror of the reference's public API for the hot path, on the C ABI.
+
+Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/include/qtree, cited file:line):
+
+  tree::estimate / estimate_alg1 / estimate_alg2 / estimate_alg3   estimate.hpp:133-309
+  tree::detail::accumulate_paths                                  estimate.hpp:88-126
+  tree::QuantTree (counts, pi, row_count, row_visited, pi_row)    quant_tree.hpp:46-84
+  quant::QuantGrid, quant::nearest                                 grid.hpp:20-61, nn.hpp:150-176
+  model::TwoFactorParams, ar1_coefficients, TwoFactorChain,
+        BrownianChain1d (+ the config-3/5 chains OuChain1d, GbmChain3d)
+  pricer::solve_stopping / solve_swing                             bdp.hpp:58-96, swing.hpp:47-129
+
+Every count, projection and price is computed by libqtree_cuda.so on the GPU;
+this module only marshals host arrays. Reference exceptions map to:
+std::invalid_argument -> ValueError, ConfigError / IoError / NumericError ->
+the classes below (errors.hpp:9-21); device failures -> NumericError("cuda: ...").
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+import os
+from dataclasses import dataclass, field
+from typing import Callable, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+
+# ---------------------------------------------------------------------------
+# errors (errors.hpp:9-21)
+# ---------------------------------------------------------------------------
+class ConfigError(RuntimeError):
+    """Bad or inconsistent run parameters (CLI exit code 1)."""
+
+
+class IoError(RuntimeError):
+    """File-format or filesystem failures (CLI exit code 2)."""
+
+
+class NumericError(RuntimeError):
+    """Numerical breakdown or device failure (CLI exit code 3)."""
+
+
+def _check(rc: int, where: str) -> None:
+    if rc == L.QT_OK:
+        return
+    msg = f"{where}: {L.last_error()}"
+    if rc == L.QT_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if rc == L.QT_ERR_CONFIG:
+        raise ConfigError(msg)
+    if rc == L.QT_ERR_IO:
+        raise IoError(msg)
+    raise NumericError(msg)
+
+
+# ---------------------------------------------------------------------------
+# enums / options (stream.hpp:16, estimate.hpp:18-36, nn.hpp:16)
+# ---------------------------------------------------------------------------
+class EngineKind(enum.IntEnum):
+    Lcg48 = 0
+    Mrg32k3a = 1
+    Xorwow = 2
+
+
+class EstimatorKind(enum.IntEnum):
+    AlgI = 0
+    AlgII = 1
+    AlgIII = 2
+
+
+class NnBackend(enum.IntEnum):
+    BruteForce = 0
+    KdTree = 1  # accepted; the device projection is exact, so results are identical
+
+
+@dataclass
+class BuildPhases:
+    simulate_ms: float = 0.0
+    nn_ms: float = 0.0
+    merge_ms: float = 0.0
+    normalize_ms: float = 0.0
+    total_ms: float = 0.0
+
+
+@dataclass
+class EstimateOptions:
+    engine: EngineKind = EngineKind.Mrg32k3a
+    seed: int = 12345
+    workers: int = 1          # accepted and ignored (the device decides the parallelism)
+    nn: NnBackend = NnBackend.BruteForce
+    phases: BuildPhases | None = None
+    devices: int = 1          # GPUs of this process to shard over (one NCCL all-reduce)
+
+
+# ---------------------------------------------------------------------------
+# model (two_factor.hpp, chains.hpp)
+# ---------------------------------------------------------------------------
+@dataclass
+class TwoFactorParams:
+    s0: float = 100.0
+    sigma1: float = 0.5
+    sigma2: float = 0.3
+    alpha1: float = 1.0
+    alpha2: float = 4.0
+    rho: float = 0.0
+    r: float = 0.0
+    strike: float = 100.0
+    horizon: float = 1.0
+    steps: int = 365
+
+    def c(self, gbm_rho=(0.0, 0.0, 0.0)) -> L.QtModelParams:
+        return L.QtModelParams(self.s0, self.sigma1, self.sigma2, self.alpha1, self.alpha2,
+                               self.rho, self.r, self.strike, self.horizon, int(self.steps),
+                               (C.c_double * 3)(*gbm_rho))
+
+
+CHAIN_BROWNIAN_1D, CHAIN_TWO_FACTOR, CHAIN_OU_1D, CHAIN_GBM_3D = 0, 1, 2, 3
+
+
+class _Chain:
+    kind: int
+    _dim: int
+
+    def __init__(self, params: TwoFactorParams, gbm_rho=(0.0, 0.0, 0.0)):
+        self.params = params
+        self.gbm_rho = tuple(gbm_rho)
+        n = int(params.steps)
+        self.step_coef = np.zeros(max(n, 0) * 6, np.float64)
+        self.marg_coef = np.zeros((max(n, 0) + 1) * 6, np.float64)
+        p = params.c(self.gbm_rho)
+        _check(L.lib().qt_chain_coefficients(self.kind, C.byref(p), _f(self.step_coef),
+                                              _f(self.marg_coef)), type(self).__name__)
+
+    def dim(self) -> int:
+        return self._dim
+
+    def layers(self) -> int:
+        return int(self.params.steps)
+
+    def normals_per_step(self) -> int:
+        return self._dim
+
+    def dt(self) -> float:
+        return self.params.horizon / self.params.steps
+
+    def time(self, k: int) -> float:
+        return k * self.dt()
+
+    def c(self) -> L.QtChain:
+        return L.QtChain(self.kind, self.layers(), _f(self.step_coef), _f(self.marg_coef))
+
+
+class BrownianChain1d(_Chain):
+    """X_{k+1} = X_k + sqrt(dt) eps (chains.hpp:68-95)."""
+    kind, _dim = CHAIN_BROWNIAN_1D, 1
+
+    def __init__(self, steps: int, horizon: float = 1.0):
+        super().__init__(TwoFactorParams(steps=steps, horizon=horizon))
+
+
+class TwoFactorChain(_Chain):
+    """Exact AR(1) form of the 2-factor OU pair (chains.hpp:30-64)."""
+    kind, _dim = CHAIN_TWO_FACTOR, 2
+
+    def __init__(self, params: TwoFactorParams):
+        super().__init__(params)
+
+
+class OuChain1d(_Chain):
+    """Config 3: factor 1 of TwoFactorChain (a = e^{-alpha1 dt}, l11)."""
+    kind, _dim = CHAIN_OU_1D, 1
+
+    def __init__(self, params: TwoFactorParams):
+        super().__init__(params)
+
+
+class GbmChain3d(_Chain):
+    """Config 5: 3-D correlated Brownian log-state, X' = X + sqrt(dt) L eps."""
+    kind, _dim = CHAIN_GBM_3D, 3
+
+    def __init__(self, steps: int, horizon: float = 1.0, rho=(0.0, 0.0, 0.0)):
+        super().__init__(TwoFactorParams(steps=steps, horizon=horizon), gbm_rho=rho)
+
+
+def ar1_coefficients(p: TwoFactorParams) -> TwoFactorParams:
+    """Ar1Spec::from_params validation (two_factor.hpp:90-101); the chain keeps the params."""
+    TwoFactorChain(p)
+    return p
+
+
+# ---------------------------------------------------------------------------
+# grids (grid.hpp)
+# ---------------------------------------------------------------------------
+class QuantGrid:
+    """N points in R^d, row-major FP64 (grid.hpp:20-61). Validity (finite,
+    distinct) is enforced by the library when a grid is used."""
+
+    def __init__(self, dim: int, points):
+        self._dim = int(dim)
+        self.points = np.ascontiguousarray(points, dtype=np.float64).reshape(-1)
+        if self._dim < 1:
+            raise NumericError("grid: dimension must be >= 1")
+        if self.points.size == 0 or self.points.size % self._dim:
+            raise NumericError("grid: point data size is not a positive multiple of dim")
+        if not np.all(np.isfinite(self.points)):
+            raise NumericError("grid: non-finite point coordinate")
+
+    def dim(self) -> int:
+        return self._dim
+
+    def size(self) -> int:
+        return self.points.size // self._dim
+
+    def point(self, i: int) -> np.ndarray:
+        return self.points[i * self._dim:(i + 1) * self._dim]
+
+    def data(self) -> np.ndarray:
+        return self.points
+
+    def __eq__(self, o) -> bool:
+        return isinstance(o, QuantGrid) and self._dim == o._dim and np.array_equal(
+            self.points, o.points)
+
+
+def _f(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _u(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_uint64))
+
+
+class _GridPack:
+    """Flattened layers 1..n for qt_grids (keeps the arrays alive)."""
+
+    def __init__(self, chain: _Chain, grids: Sequence[QuantGrid]):
+        if len(grids) != chain.layers():
+            raise ValueError("estimate: need one grid per layer 1..n")
+        for g in grids:
+            if g.dim() != chain.dim():
+                raise ValueError("estimate: grid dimension mismatch")
+        self.sizes = np.array([1] + [g.size() for g in grids], np.uint64)
+        self.points = np.ascontiguousarray(np.concatenate([g.data() for g in grids]))
+        self.s = L.QtGrids(chain.dim(), chain.layers(), _u(self.sizes), _f(self.points))
+
+
+def layout(sizes) -> tuple[int, int]:
+    sizes = [int(s) for s in sizes]
+    return sum(sizes), sum(sizes[k - 1] * sizes[k] for k in range(1, len(sizes)))
+
+
+# ---------------------------------------------------------------------------
+# tree (quant_tree.hpp)
+# ---------------------------------------------------------------------------
+@dataclass
+class CountMatrixSet:
+    visits: list = field(default_factory=list)  # layer 0..n, u64 arrays
+    joint: list = field(default_factory=list)   # transition 1..n, row-major N_{k-1} x N_k
+
+
+class QuantTree:
+    """Grids 0..n, counts, dense FP64 pi and M (quant_tree.hpp:46-84)."""
+
+    def __init__(self, grids, sizes, visits, joint, pi, samples):
+        self.grids = grids
+        self.sizes = np.asarray(sizes, np.uint64)
+        self.flat_visits, self.flat_joint, self.flat_pi = visits, joint, pi
+        self.samples = int(samples)
+        self.counts = CountMatrixSet()
+        self.pi = []
+        vo = jo = 0
+        for k, s in enumerate(self.sizes):
+            self.counts.visits.append(visits[vo:vo + int(s)])
+            vo += int(s)
+            if k:
+                r = int(self.sizes[k - 1])
+                self.counts.joint.append(joint[jo:jo + r * int(s)])
+                self.pi.append(pi[jo:jo + r * int(s)])
+                jo += r * int(s)
+
+    def layers(self) -> int:
+        return len(self.pi)
+
+    def layer_size(self, k: int) -> int:
+        return int(self.sizes[k])
+
+    def row_count(self, k: int, i: int) -> int:
+        return int(self.counts.visits[k - 1][i])
+
+    def row_visited(self, k: int, i: int) -> bool:
+        return self.row_count(k, i) > 0
+
+    def pi_row(self, k: int, i: int) -> np.ndarray:
+        c = self.layer_size(k)
+        return self.pi[k - 1][i * c:(i + 1) * c]
+
+
+def _estimate(kind: int, chain: _Chain, grids: Sequence[QuantGrid], paths: int,
+              opt: EstimateOptions | None, normals=None) -> QuantTree:
+    opt = opt or EstimateOptions()
+    if kind in (EstimatorKind.AlgII, EstimatorKind.AlgIII) and opt.workers < 1:
+        raise ValueError(f"estimate_alg{int(kind) + 1}: workers must be >= 1")
+    if paths <= 0:
+        raise ValueError("estimate: need at least one path")
+    gp = _GridPack(chain, grids)
+    nvis, njoint = layout(gp.sizes)
+    visits = np.zeros(nvis, np.uint64)
+    joint = np.zeros(njoint, np.uint64)
+    pi = np.zeros(njoint, np.float64)
+    ph = np.zeros(5, np.float64)
+    ch = chain.c()
+    if normals is None:
+        rc = L.lib().qt_estimate(int(kind), C.byref(ch), C.byref(gp.s), int(paths),
+                                 int(opt.engine), int(opt.seed), int(opt.devices), _u(visits),
+                                 _u(joint), _f(pi), _f(ph))
+    else:
+        nrm = np.ascontiguousarray(normals, dtype=np.float64)
+        rc = L.lib().qt_estimate_normals(int(kind), C.byref(ch), C.byref(gp.s), int(paths),
+                                         _f(nrm), _u(visits), _u(joint), _f(pi))
+    _check(rc, "estimate")
+    if opt.phases is not None:
+        opt.phases.simulate_ms, opt.phases.nn_ms, opt.phases.merge_ms, \
+            opt.phases.normalize_ms, opt.phases.total_ms = (float(x) for x in ph)
+    x0 = QuantGrid(chain.dim(), np.zeros(chain.dim()))
+    return QuantTree([x0] + list(grids), gp.sizes, visits, joint, pi, paths)
+
+
+def estimate_alg1(chain, grids, paths, opt=None) -> QuantTree:
+    """Algorithm I (estimate.hpp:133-157): pathwise estimation."""
+    return _estimate(EstimatorKind.AlgI, chain, grids, paths, opt)
+
+
+def estimate_alg2(chain, grids, paths, opt=None) -> QuantTree:
+    """Algorithm II (estimate.hpp:163-207): path-parallel; identical counts to Alg I."""
+    return _estimate(EstimatorKind.AlgII, chain, grids, paths, opt)
+
+
+def estimate_alg3(chain, grids, samples_per_layer, opt=None) -> QuantTree:
+    """Algorithm III (estimate.hpp:213-296): layer-parallel pair sampling."""
+    return _estimate(EstimatorKind.AlgIII, chain, grids, samples_per_layer, opt)
+
+
+def estimate(kind, chain, grids, paths, opt=None) -> QuantTree:
+    """Dispatch by estimator kind (estimate.hpp:299-309)."""
+    if int(kind) not in (0, 1, 2):
+        raise ValueError("estimate: unknown estimator kind")
+    return _estimate(EstimatorKind(int(kind)), chain, grids, paths, opt)
+
+
+def estimate_with_normals(kind, chain, grids, paths, normals) -> QuantTree:
+    """Parity mode: the estimator consumes caller-supplied normals."""
+    return _estimate(EstimatorKind(int(kind)), chain, grids, paths, None, normals=normals)
+
+
+def accumulate_paths(chain, grids, engine, seed, first, count, total):
+    """detail::accumulate_paths over paths [first, first+count) of `total`
+    (estimate.hpp:88-126). Returns flat (visits, joint)."""
+    gp = _GridPack(chain, grids)
+    nvis, njoint = layout(gp.sizes)
+    visits = np.zeros(nvis, np.uint64)
+    joint = np.zeros(njoint, np.uint64)
+    ch = chain.c()
+    _check(L.lib().qt_accumulate_paths(C.byref(ch), C.byref(gp.s), int(engine), int(seed),
+                                       int(first), int(count), int(total), _u(visits),
+                                       _u(joint)), "accumulate_paths")
+    return visits, joint
+
+
+def nearest(grid: QuantGrid, queries) -> np.ndarray:
+    """Batch NnIndex::nearest (nn.hpp:18-46): exact, smallest index on ties."""
+    q = np.ascontiguousarray(queries, dtype=np.float64).reshape(-1)
+    if q.size % grid.dim():
+        raise ValueError("nearest: query dimension mismatch")
+    out = np.zeros(q.size // grid.dim(), np.uint64)
+    _check(L.lib().qt_nearest(grid.dim(), grid.size(), _f(grid.points), out.size, _f(q),
+                              _u(out)), "nearest")
+    return out
+
+
+def path_normals(engine, seed, normals_per_path, first, count) -> np.ndarray:
+    out = np.zeros(int(count) * int(normals_per_path), np.float64)
+    _check(L.lib().qt_path_normals(int(engine), int(seed), int(normals_per_path), int(first),
+                                   int(count), _f(out)), "path_normals")
+    return out
+
+
+def uniforms(engine, seed, offset, count) -> np.ndarray:
+    out = np.zeros(int(count), np.float64)
+    _check(L.lib().qt_uniforms(int(engine), int(seed), int(offset), int(count), _f(out)),
+           "uniforms")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# pricer (bdp.hpp, swing.hpp)
+# ---------------------------------------------------------------------------
+NodePayoff = Callable[[int, np.ndarray], float]
+
+
+def tabulate(tree: QuantTree, payoff) -> np.ndarray:
+    """NodePayoff -> phi laid out like visits. Accepts a callable
+    f(layer, node_coords) (bdp.hpp:17) or an already flat table."""
+    if not callable(payoff):
+        phi = np.ascontiguousarray(payoff, dtype=np.float64)
+        if phi.size != int(tree.sizes.sum()):
+            raise ValueError("payoff table length mismatch")
+        return phi
+    out = []
+    for k in range(tree.layers() + 1):
+        g = tree.grids[k]
+        out.extend(float(payoff(k, g.point(i))) for i in range(g.size()))
+    return np.array(out, np.float64)
+
+
+@dataclass
+class StoppingResult:
+    value: list
+    exercise: list
+    price: float
+
+
+@dataclass
+class SwingResult:
+    q_min: int
+    q_max: int
+    m_lo: list
+    m_count: list
+    value: list
+    price: float
+
+
+def solve_stopping(tree: QuantTree, payoff) -> StoppingResult:
+    """V_k = max(phi_k, E(V_{k+1}|node)), absorbing unvisited nodes (bdp.hpp:58-96)."""
+    if tree is None or payoff is None:
+        raise ValueError("solve_stopping: incomplete problem")
+    phi = tabulate(tree, payoff)
+    n = tree.layers()
+    value = np.zeros(phi.size, np.float64)
+    ex = np.zeros(phi.size, np.uint8)
+    price = C.c_double()
+    _check(L.lib().qt_bdp_stopping(n, _u(tree.sizes), _u(tree.flat_visits), _f(tree.flat_pi),
+                                   _f(phi), _f(value), ex.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                   C.byref(price)), "solve_stopping")
+    vs, es, o = [], [], 0
+    for k in range(n + 1):
+        s = tree.layer_size(k)
+        vs.append(value[o:o + s])
+        es.append(ex[o:o + s])
+        o += s
+    return StoppingResult(vs, es, price.value)
+
+
+def swing_window(n: int, qmin: int, qmax: int):
+    lo = [max(0, qmin - (n - k)) for k in range(n + 1)]
+    cnt = [min(k, qmax) - lo[k] + 1 for k in range(n + 1)]
+    return lo, cnt
+
+
+def solve_swing(tree: QuantTree, payoff, q_min: int, q_max: int) -> SwingResult:
+    """Bang-bang swing recursion over (layer, node, consumption) (swing.hpp:47-129)."""
+    if tree is None or payoff is None:
+        raise ValueError("solve_swing: incomplete problem")
+    phi = tabulate(tree, payoff)
+    n = tree.layers()
+    lo, cnt = swing_window(n, q_min, q_max)
+    total = sum(max(c, 0) * tree.layer_size(k) for k, c in enumerate(cnt))
+    vals = np.zeros(max(total, 1), np.float64)
+    price = C.c_double()
+    _check(L.lib().qt_bdp_swing(n, _u(tree.sizes), _u(tree.flat_visits), _f(tree.flat_pi),
+                                _f(phi), int(q_min), int(q_max), C.byref(price), _f(vals)),
+           "solve_swing")
+    value, o = [], 0
+    for k in range(n + 1):
+        s = cnt[k] * tree.layer_size(k)
+        value.append(vals[o:o + s])
+        o += s
+    return SwingResult(q_min, q_max, lo, cnt, value, price.value)
+
+
+# ---------------------------------------------------------------------------
+# grid inputs: the reference's per-layer mappings (pipeline.hpp:27-77) of the
+# standard-normal Lloyd base quantizers shipped in data/base_grids.npz
+# ---------------------------------------------------------------------------
+_DATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "base_grids.npz")
+
+
+def base_grid(grid_size: int, dim: int) -> np.ndarray:
+    key = f"n{grid_size}_d{dim}"
+    with np.load(_DATA) as z:
+        if key not in z:
+            raise ValueError(f"no base quantizer {key} in {_DATA} (grid construction is out of "
+                             "scope for the device path; see DESIGN.md)")
+        return np.array(z[key])
+
+
+def _cholesky2_marginal(p: TwoFactorParams, t: float):
+    c11 = -math.expm1(-2.0 * p.alpha1 * t) / (2.0 * p.alpha1)
+    c22 = -math.expm1(-2.0 * p.alpha2 * t) / (2.0 * p.alpha2)
+    c12 = -p.rho * math.expm1(-(p.alpha1 + p.alpha2) * t) / (p.alpha1 + p.alpha2)
+    l11 = math.sqrt(c11)
+    l21 = c12 / l11 if l11 > 0.0 else 0.0
+    rem = c22 - l21 * l21
+    return l11, l21, math.sqrt(max(0.0, rem))
+
+
+def build_brownian_grids(chain: BrownianChain1d, grid_size: int):
+    """sqrt(t_k) times the N(0,1) base grid (pipeline.hpp:57-77)."""
+    base = base_grid(grid_size, 1)
+    return [QuantGrid(1, base * math.sqrt(chain.time(k))) for k in range(1, chain.layers() + 1)]
+
+
+def build_two_factor_grids(chain: TwoFactorChain, grid_size: int):
+    """Base grid mapped by the marginal Cholesky factor per layer (pipeline.hpp:27-53)."""
+    base = base_grid(grid_size, 2).reshape(-1, 2)
+    p = chain.params
+    out = []
+    for k in range(1, chain.layers() + 1):
+        l11, l21, l22 = _cholesky2_marginal(p, k * (p.horizon / p.steps))
+        z1, z2 = base[:, 0], base[:, 1]
+        pts = np.stack([l11 * z1, l21 * z1 + l22 * z2], axis=1)
+        out.append(QuantGrid(2, pts))
+    return out
+
+
+def build_ou_grids(chain: OuChain1d, grid_size: int):
+    """Config 3: base grid times the factor-1 marginal sd of each layer."""
+    base = base_grid(grid_size, 1)
+    p = chain.params
+    return [QuantGrid(1, base * _cholesky2_marginal(p, k * (p.horizon / p.steps))[0])
+            for k in range(1, chain.layers() + 1)]
+
+
+def build_gbm_grids(chain: GbmChain3d, grid_size: int):
+    """Config 5: base grid mapped by sqrt(t_k) L per layer."""
+    base = base_grid(grid_size, 3).reshape(-1, 3)
+    m = chain.marg_coef.reshape(-1, 6)
+    out = []
+    for k in range(1, chain.layers() + 1):
+        c = m[k]
+        z0, z1, z2 = base[:, 0], base[:, 1], base[:, 2]
+        pts = np.stack([c[0] * z0, c[1] * z0 + c[2] * z1, (c[3] * z0 + c[4] * z1) + c[5] * z2],
+                       axis=1)
+        out.append(QuantGrid(3, pts))
+    return out

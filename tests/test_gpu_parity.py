@@ -1,0 +1,293 @@
+"""Parity of the CUDA path against the CPU checker, through the C ABI.
+
+Bar: bit-exact cell indices, counts, visits and pi (integer / index work and
+a correctly rounded division), bit-exact BDP values (sequential row sums in
+the reference's order). The normals themselves come from CUDA log/sin/cos
+(<= 1-2 ulp vs glibc): with reference normals supplied (parity mode) counts
+are exact by construction; with the in-kernel stream they are checked
+bit-exact on the seeded configs below and any mismatch fails the test."""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from pyoracle import (ALG_I, ALG_II, ALG_III, CHAIN_BROWNIAN1D, CHAIN_GBM3D, CHAIN_OU1D,
+                      CHAIN_TWO_FACTOR, ChainSpec, PAYOFF_PUT, PAYOFF_SWING)
+
+pytestmark = pytest.mark.gpu
+
+ENGINES = ("lcg48", "mrg32k3a", "xorwow")
+TAGS = {"bm": CHAIN_BROWNIAN1D, "tf": CHAIN_TWO_FACTOR, "ou": CHAIN_OU1D, "gbm": CHAIN_GBM3D}
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def Q():
+    from paper_1101_3228_b200 import qtree
+    return qtree
+
+
+def product_chain(spec: ChainSpec):
+    q = Q()
+    p = q.TwoFactorParams(s0=spec.s0, sigma1=spec.sigma1, sigma2=spec.sigma2, alpha1=spec.alpha1,
+                          alpha2=spec.alpha2, rho=spec.rho, r=spec.r, strike=spec.strike,
+                          horizon=spec.horizon, steps=spec.steps)
+    if spec.kind == CHAIN_BROWNIAN1D:
+        return q.BrownianChain1d(spec.steps, spec.horizon)
+    if spec.kind == CHAIN_TWO_FACTOR:
+        return q.TwoFactorChain(p)
+    if spec.kind == CHAIN_OU1D:
+        return q.OuChain1d(p)
+    return q.GbmChain3d(spec.steps, spec.horizon, spec.gbm_rho)
+
+
+def product_grids(spec, sizes, pts):
+    q = Q()
+    out, o = [], 0
+    for s in sizes[1:]:
+        s = int(s)
+        out.append(q.QuantGrid(spec.dim, pts[o:o + s * spec.dim]))
+        o += s * spec.dim
+    return out
+
+
+def small_spec(kind, steps=5):
+    return ChainSpec(kind, steps, sigma1=0.4, sigma2=0.7, alpha1=0.8, alpha2=3.5, rho=0.3,
+                     gbm_rho=(0.3, 0.1, -0.2))
+
+
+def assert_tree_equal(t, visits, joint, pi):
+    assert np.array_equal(t.flat_joint, joint)
+    assert np.array_equal(t.flat_visits, visits)
+    assert np.array_equal(t.flat_pi, pi)
+
+
+# --- RNG ----------------------------------------------------------------------
+def test_uniforms_bit_exact(gpu, oracle):
+    q = Q()
+    for e in (0, 1):
+        for off in (0, 1, 12345, 10**9 + 7, 2**40 + 3):
+            # block substream `off` of size 1 starts at serial draw `off` (stream.hpp:156-158)
+            ref = oracle.uniforms(e, 12345, 257, False, off + 1, off, 1)
+            got = q.uniforms(e, 12345, off, 257)
+            assert np.array_equal(got, ref), (e, off)
+
+
+def test_normals_close_to_glibc(gpu, oracle):
+    """In-kernel Box-Muller vs glibc: report the ulp histogram; every value
+    within 2 ulp; the vast majority bit-identical."""
+    q = Q()
+    for e in range(3):
+        ref = oracle.path_normals(e, 12345, 50, 1000, 20000, 10**9)
+        got = q.path_normals(e, 12345, 50, 1000, 20000)
+        ulp = np.abs(got.view(np.int64) - ref.view(np.int64))
+        assert ulp.max() <= 4, (e, int(ulp.max()))
+        assert np.mean(ulp == 0) > 0.5, (e, float(np.mean(ulp == 0)))
+
+
+# --- estimator, parity mode (reference normals in) -------------------------------
+@pytest.mark.parametrize("tag", list(TAGS))
+@pytest.mark.parametrize("alg", [ALG_I, ALG_II, ALG_III])
+def test_normals_in_bit_exact(gpu, oracle, golden, tag, alg):
+    st = golden["small_trees"]
+    spec = small_spec(TAGS[tag])
+    sizes, pts = st[f"{tag}_sizes"], st[f"{tag}_pts"]
+    n, d = spec.steps, spec.dim
+    M = 3000
+    if alg == ALG_III:
+        normals = oracle.path_normals(1, 42, 2 * d, 0, n * M, n * M)
+    else:
+        normals = oracle.path_normals(1, 42, n * d, 0, M, M)
+    ref = oracle.estimate(alg, spec, sizes, pts, M, engine=1, seed=42, workers=2)
+    t = Q().estimate_with_normals(alg, product_chain(spec), product_grids(spec, sizes, pts), M,
+                                  normals)
+    assert_tree_equal(t, ref.visits, ref.joint, ref.pi)
+
+
+# --- estimator, in-kernel stream ---------------------------------------------------
+@pytest.mark.parametrize("tag", list(TAGS))
+def test_small_trees_all_engines(gpu, golden, tag):
+    st = golden["small_trees"]
+    spec = small_spec(TAGS[tag])
+    sizes, pts = st[f"{tag}_sizes"], st[f"{tag}_pts"]
+    q = Q()
+    ch, grids = product_chain(spec), product_grids(spec, sizes, pts)
+    for alg, an in ((ALG_I, "alg1"), (ALG_III, "alg3")):
+        for e, en in enumerate(ENGINES):
+            t = q.estimate(alg, ch, grids, 4000, q.EstimateOptions(engine=e, seed=99))
+            assert_tree_equal(t, st[f"{tag}_{an}_{en}_visits"], st[f"{tag}_{an}_{en}_joint"],
+                              st[f"{tag}_{an}_{en}_pi"])
+    v, j = q.accumulate_paths(ch, grids, 1, 12345, 777, 300, 10**6)
+    assert np.array_equal(v, st[f"{tag}_window_visits"])
+    assert np.array_equal(j, st[f"{tag}_window_joint"])
+
+
+def test_alg2_equals_alg1_and_device_sharding(gpu, golden):
+    # worker-count invariance (test_tree.cpp:128-152) -> shard invariance
+    st = golden["small_trees"]
+    spec = small_spec(CHAIN_TWO_FACTOR)
+    q = Q()
+    ch, grids = product_chain(spec), product_grids(spec, st["tf_sizes"], st["tf_pts"])
+    base = q.estimate_alg1(ch, grids, 4000, q.EstimateOptions(seed=99))
+    t = q.estimate_alg2(ch, grids, 4000, q.EstimateOptions(seed=99, workers=8))
+    assert_tree_equal(t, base.flat_visits, base.flat_joint, base.flat_pi)
+    import torch
+    from paper_1101_3228_b200.device import Plan
+    plan = Plan(ch, grids, 0)
+    for shards in (1, 2, 3, 8):
+        joint = plan.zeros_joint()
+        for s in range(shards):
+            b, e = 4000 * s // shards, 4000 * (s + 1) // shards
+            plan.count(1, 1, 99, b, e - b, 4000, joint)
+        torch.cuda.synchronize()
+        assert np.array_equal(joint.cpu().numpy().view(np.uint64), base.flat_joint)
+
+
+def test_c1_config_bit_exact(gpu, oracle, golden):
+    """BASELINE config 1: 1-D BS put, n=10, N=100, M=1e6, MRG32k3a seed 12345."""
+    q = Q()
+    cf = golden["configs"]
+    ch = q.BrownianChain1d(10)
+    grids = q.build_brownian_grids(ch, 100)
+    t = q.estimate_alg2(ch, grids, 10**6)
+    assert np.array_equal(t.flat_visits, cf["c1_visits"])
+    assert sha(t.flat_joint) == str(cf["c1_joint_sha"])
+    assert sha(t.flat_pi) == str(cf["c1_pi_sha"])
+    spec = ChainSpec(CHAIN_BROWNIAN1D, 10, sigma1=0.2, r=0.05)
+    pts_all = np.concatenate([[0.0]] + [g.data() for g in grids])
+    phi = oracle.payoff_table(spec, PAYOFF_PUT, t.sizes, pts_all)
+    res = q.solve_stopping(t, phi)
+    assert res.price == float(cf["c1_put_price"])
+
+
+def test_c2_windows_bit_exact(gpu, golden):
+    """BASELINE config 2 (n=50, N=500, M=1e9): three 20000-path windows."""
+    q = Q()
+    cf = golden["configs"]
+    ch = q.BrownianChain1d(50)
+    grids = q.build_brownian_grids(ch, 500)
+    for first in (0, 123456789, 999980000):
+        v, j = q.accumulate_paths(ch, grids, 1, 12345, first, 20000, 10**9)
+        assert np.array_equal(v, cf[f"c2_win{first}_visits"]), first
+        assert sha(j) == str(cf[f"c2_win{first}_joint_sha"]), first
+
+
+def test_c2_random_window_vs_oracle(gpu, oracle):
+    q = Q()
+    ch = q.BrownianChain1d(50)
+    grids = q.build_brownian_grids(ch, 500)
+    spec = ChainSpec(CHAIN_BROWNIAN1D, 50)
+    sizes = np.array([1] + [500] * 50, np.uint64)
+    pts = np.concatenate([g.data() for g in grids])
+    rng = np.random.default_rng(2026)
+    for first in rng.integers(0, 10**9 - 50000, size=2):
+        v, j = q.accumulate_paths(ch, grids, 1, 12345, int(first), 50000, 10**9)
+        rv, rj = oracle.accumulate_paths(spec, sizes, pts, 1, 12345, int(first), 50000, 10**9)
+        assert np.array_equal(v, rv) and np.array_equal(j, rj), int(first)
+
+
+def test_c3_c4_shapes_vs_oracle(gpu, oracle):
+    q = Q()
+    # C3: OU 1-D, Alg III, n = 365, N = 200 (reduced M)
+    p = q.TwoFactorParams(sigma1=0.5, alpha1=1.0, sigma2=0.0, steps=365)
+    ch = q.OuChain1d(p)
+    grids = q.build_ou_grids(ch, 200)
+    spec = ChainSpec(CHAIN_OU1D, 365, sigma1=0.5, alpha1=1.0, sigma2=0.0)
+    sizes = np.array([1] + [200] * 365, np.uint64)
+    pts = np.concatenate([g.data() for g in grids])
+    t = q.estimate_alg3(ch, grids, 2000)
+    r = oracle.estimate(ALG_III, spec, sizes, pts, 2000, workers=8)
+    assert_tree_equal(t, r.visits, r.joint, r.pi)
+    # C4: 2-factor, n = 365, N = 1000 (reduced M)
+    tf = q.TwoFactorChain(q.TwoFactorParams())
+    g4 = q.build_two_factor_grids(tf, 1000)
+    spec4 = ChainSpec(CHAIN_TWO_FACTOR, 365)
+    s4 = np.array([1] + [1000] * 365, np.uint64)
+    p4 = np.concatenate([g.data() for g in g4])
+    v, j = q.accumulate_paths(tf, g4, 1, 12345, 5000, 600, 10**8)
+    rv, rj = oracle.accumulate_paths(spec4, s4, p4, 1, 12345, 5000, 600, 10**8)
+    assert np.array_equal(v, rv) and np.array_equal(j, rj)
+
+
+def test_conservation_at_scale(gpu):
+    """Sum of counts per transition = M at a size the oracle cannot run."""
+    import torch
+    q = Q()
+    from paper_1101_3228_b200.device import Plan
+    ch = q.BrownianChain1d(50)
+    plan = Plan(ch, q.build_brownian_grids(ch, 500), 0)
+    M = 10**8
+    joint = plan.zeros_joint()
+    plan.count(1, 1, 12345, 0, M, M, joint)
+    visits = torch.zeros(plan.n_visits, dtype=torch.int64, device="cuda")
+    pi = torch.zeros(plan.n_joint, dtype=torch.float64, device="cuda")
+    plan.finalize(1, M, joint, visits, pi)
+    torch.cuda.synchronize()
+    j = joint.cpu().numpy().view(np.uint64)
+    assert int(j[:500].sum()) == M
+    rest = j[500:].reshape(49, 500, 500)
+    assert np.all(rest.sum(axis=(1, 2)) == M)
+    v = visits.cpu().numpy().view(np.uint64)
+    assert v[0] == M and np.all(v[1:].reshape(50, 500).sum(1) == M)
+
+
+# --- projection -----------------------------------------------------------------------
+def test_nearest_matches_reference_including_edges(gpu, oracle):
+    q = Q()
+    rng = np.random.default_rng(11)
+    for d, N in ((1, 1), (1, 2), (1, 500), (1, 4000), (2, 1000), (3, 400)):
+        pts = rng.standard_normal(N * d)
+        qs = [rng.standard_normal(20000 * d) * 1.5]
+        if d == 1:
+            s = np.sort(pts)
+            mids = (s[:-1] + s[1:]) / 2 if N > 1 else np.array([])
+            qs += [pts, mids, np.nextafter(mids, np.inf), np.nextafter(mids, -np.inf),
+                   np.array([-1e300, 1e300, 1e200, -1e-300, 0.0, -0.0, np.inf, -np.inf, np.nan])]
+        else:
+            qs += [pts]
+        qq = np.concatenate([x.reshape(-1) for x in qs])
+        got = q.nearest(q.QuantGrid(d, pts), qq)
+        ref = oracle.nearest(d, pts, qq)
+        assert np.array_equal(got, ref), (d, N)
+    # symmetric tie -> smallest index (test_quant.cpp:42-45)
+    assert q.nearest(q.QuantGrid(2, [0.0, 0.0, 1.0, 0.0]), [0.5, 0.0]).tolist() == [0]
+    assert q.nearest(q.QuantGrid(1, [1.0, -1.0]), [0.0]).tolist() == [0]
+    assert q.nearest(q.QuantGrid(1, [-1.0, 1.0]), [0.0]).tolist() == [0]
+
+
+# --- pricer ---------------------------------------------------------------------------
+def test_bdp_matches_golden_exactly(gpu, golden):
+    q = Q()
+    pr = golden["pricing"]
+    for case in range(4):
+        g = {k.split("_", 1)[1]: v for k, v in pr.items() if k.startswith(f"case{case}_")}
+        sizes = g["sizes"]
+        t = q.QuantTree([q.QuantGrid(1, np.arange(int(s), dtype=np.float64)) for s in sizes],
+                        sizes, g["visits"], g["joint"], g["pi"], 1)
+        res = q.solve_stopping(t, g["phi"])
+        assert res.price == float(g["stop_price"])
+        assert np.array_equal(np.concatenate(res.value), g["stop_value"])
+        assert np.array_equal(np.concatenate(res.exercise), g["stop_exercise"])
+        qmin, qmax = (int(x) for x in g["swing_q"])
+        sw = q.solve_swing(t, g["phi"], qmin, qmax)
+        assert sw.price == float(g["swing_price"])
+        assert np.array_equal(np.concatenate(sw.value), g["swing_values"])
+    with pytest.raises(q.ConfigError):
+        q.solve_swing(t, g["phi"], 3, 2)
+
+
+def test_swing_on_estimated_tree(gpu, oracle):
+    q = Q()
+    ch = q.BrownianChain1d(10)
+    grids = q.build_brownian_grids(ch, 100)
+    t = q.estimate_alg1(ch, grids, 200000)
+    spec = ChainSpec(CHAIN_BROWNIAN1D, 10, sigma1=0.2, r=0.05)
+    pts_all = np.concatenate([[0.0]] + [g.data() for g in grids])
+    phi = oracle.payoff_table(spec, PAYOFF_SWING, t.sizes, pts_all)
+    sp = q.solve_swing(t, phi, 2, 6)
+    rp = oracle.solve_swing(t.sizes, t.flat_visits, t.flat_pi, phi, 2, 6)
+    assert sp.price == rp
