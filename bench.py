@@ -58,13 +58,15 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profiled_traffic(config: str):
-    """dram bytes per launch of the path kernel from the committed ncu capture."""
+def profiled_traffic(config: str, transitions: int):
+    """dram__bytes_read + dram__bytes_write of one path-kernel launch, scaled
+    from the committed ncu --set full capture (profiles/traffic.json)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         with open(p) as f:
-            d = json.load(f)
-        return d.get(config)
+            d = json.load(f).get(config)
+        if d:
+            return d["bytes_per_transition"] * transitions / 1e9  # GB per launch
     return None
 
 
@@ -378,7 +380,10 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": f"paths sharded over {world} GPU(s), one NCCL reduce",
                    "l2": "flushed between timed steps (256 MiB write)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": profiled_traffic(args.config),
+                     "frac": achieved / peak,
+                     "traffic": profiled_traffic(args.config, kern_units),
+                     "traffic_unit": "GB per launch (ncu dram read+write)",
+                     "algorithmic_gb_per_launch": 16.0 * kern_units / 1e9,
                      "kernel": "k_paths (fused RNG + step + projection + count)",
                      "kernel_ms": t_kern, "peak_source": peak_src,
                      "algorithmic_bytes": "16 B per transition (u64 counter read-modify-write)"},
