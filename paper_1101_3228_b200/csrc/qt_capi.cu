@@ -298,90 +298,146 @@ void check_grid(int dim, uint64_t npts, const double* pts, int layer) {
       raise(QT_ERR_NUMERIC, "grid: duplicate points (layer " + std::to_string(layer) + ")");
 }
 
-// Bytes of one layer table.
-std::vector<uint8_t> build_table(int dim, uint64_t npts, const double* pts, const double* step,
-                                 const double* marg_prev, uint64_t joff, uint64_t voff,
-                                 uint64_t n_prev, uint32_t layer) {
+// Ordered 64-bit key of a double: monotone in numeric order (-0 just below +0).
+uint64_t dkey(double x) {
+  uint64_t b;
+  std::memcpy(&b, &x, 8);
+  return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+double dfromkey(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & ~(1ull << 63)) : ~k;
+  double x;
+  std::memcpy(&x, &b, 8);
+  return x;
+}
+
+// The reference's pairwise choice between sorted neighbours vl < vh for a
+// query x in [vl, vh]: separately rounded d2 (nn.hpp:38-45), smaller index on
+// ties (strict < in index order).
+bool choose_hi(double x, double vl, double vh, uint32_t ol, uint32_t oh) {
+  volatile double dl = x - vl, dh = x - vh;
+  volatile double d2l = dl * dl, d2h = dh * dh;
+  return d2h < d2l || (d2h == d2l && oh < ol);
+}
+
+struct TableBlob {
+  std::vector<uint8_t> hot;   // staged into shared memory
+  std::vector<uint8_t> cold;  // d == 1 exact-scan records (global memory only)
+};
+
+// One layer's table (layout in qt_layout.h). header.cold_off is patched by
+// the caller once the cold block's position is known.
+TableBlob build_table(int dim, uint64_t npts, const double* pts, const double* step,
+                      const double* marg_prev, uint64_t joff, uint64_t n_prev, uint32_t layer) {
   LayerTable h{};
   std::memcpy(h.step, step, sizeof h.step);
   std::memcpy(h.marg_prev, marg_prev, sizeof h.marg_prev);
   h.joff = joff;
-  h.voff = voff;
   h.n_pts = static_cast<uint32_t>(npts);
   h.n_prev = static_cast<uint32_t>(n_prev);
   h.layer = layer;
   h.dim = static_cast<uint32_t>(dim);
   h.off_rec = sizeof(LayerTable);
-  std::vector<uint8_t> out;
+  TableBlob out;
   if (dim == 1) {
     std::vector<uint32_t> ord(npts);
     std::iota(ord.begin(), ord.end(), 0u);
     std::sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) { return pts[a] < pts[b]; });
     std::vector<double> v(npts);
     for (uint64_t s = 0; s < npts; ++s) v[s] = pts[ord[s]];
-    const double lo = v.front(), hi = v.back();
     // x_safe: |x| below it rules out equal d2 between same-side neighbours
-    // (gap > 2^-51 (|x| + max|v|) suffices, 8x margin) and d2 overflow.
+    // (gap > 2^-51 (|x| + max|v|) suffices; 8x margin) and d2 overflow.
     double gmin = std::numeric_limits<double>::infinity();
     for (uint64_t s = 1; s < npts; ++s) gmin = std::min(gmin, v[s] - v[s - 1]);
-    const double vmax = std::max(std::fabs(lo), std::fabs(hi));
+    const double vmax = std::max(std::fabs(v.front()), std::fabs(v.back()));
     double x_safe;
     if (npts == 1) x_safe = vmax <= 1e150 ? 1e150 : 0.0;
-    else if (gmin >= 1e-150 && vmax <= 1e150)
-      x_safe = std::min(gmin * 0x1p48 - vmax, 1e150);
+    else if (gmin >= 1e-150 && vmax <= 1e150) x_safe = std::min(gmin * 0x1p48 - vmax, 1e150);
     else x_safe = 0.0;
-    if (!(x_safe > 0.0)) x_safe = 0.0;
-    if (npts > 65534) x_safe = 0.0;  // start[] is u16: exact scan only
-    // bucket count: grow until no bucket holds two points (cap 8N)
+    if (!(x_safe > 0.0) || npts > 65534) x_safe = 0.0;  // exact scan only
+    // decision thresholds t_c between sorted c and c+1 (bisection over doubles)
+    std::vector<double> t(npts, std::numeric_limits<double>::infinity());
+    for (uint64_t c = 0; c + 1 < npts && x_safe > 0.0; ++c) {
+      const double vl = v[c], vh = v[c + 1];
+      if (choose_hi(vl, vl, vh, ord[c], ord[c + 1]) || !choose_hi(vh, vl, vh, ord[c], ord[c + 1])) {
+        x_safe = 0.0;  // degenerate pair: keep the exact scan
+        break;
+      }
+      uint64_t klo = dkey(vl), khi = dkey(vh);
+      while (khi - klo > 1) {
+        const uint64_t mid = klo + (khi - klo) / 2;
+        if (choose_hi(dfromkey(mid), vl, vh, ord[c], ord[c + 1])) khi = mid;
+        else klo = mid;
+      }
+      t[c] = dfromkey(khi);
+    }
+    // uniform buckets over [t_0, t_{N-2}]; the fewest (multiple of N) that keep
+    // one threshold per bucket, else at most two (then a rare one-step walk)
     uint32_t nb = 1;
-    double inv_w = 0.0;
-    if (npts > 1 && npts <= 65534) {
-      for (nb = static_cast<uint32_t>(2 * npts);; nb *= 2) {
-        inv_w = static_cast<double>(nb) / (hi - lo);
-        if (!std::isfinite(inv_w)) {
-          nb = 1;
-          inv_w = 0.0;
-          break;
-        }
+    double lo = 0.0, inv_w = 0.0;
+    if (npts > 2 && x_safe > 0.0) {
+      lo = t[0];
+      const double span = t[npts - 2] - t[0];
+      uint32_t pick2 = 0;
+      for (uint32_t m = 1; m <= 8; ++m) {
+        const uint32_t cand = static_cast<uint32_t>(m * npts);
+        const double iw = static_cast<double>(cand) / span;
+        if (!std::isfinite(iw) || !(iw > 0.0)) break;
         uint32_t prev = 0xFFFFFFFFu, run = 0, worst = 0;
-        for (uint64_t s = 0; s < npts; ++s) {
-          const uint32_t b = qt::bucket_of(v[s], lo, inv_w, static_cast<double>(nb), nb);
+        for (uint64_t c = 0; c + 1 < npts; ++c) {
+          const uint32_t b = qt::bucket_of(t[c], lo, iw, static_cast<double>(cand), cand);
           run = b == prev ? run + 1 : 1;
           prev = b;
           worst = std::max(worst, run);
         }
-        if (worst <= 1 || nb >= 8 * npts) break;
+        if (worst <= 2 && !pick2) pick2 = cand;
+        if (worst <= 1 && m <= 6) {
+          nb = cand;
+          break;
+        }
+        if (m == 8) nb = pick2 ? pick2 : cand;
       }
+      if (nb > 1) inv_w = static_cast<double>(nb) / span;
+      else nb = 1;
     }
     h.lo = lo;
     h.inv_w = inv_w;
     h.x_safe = x_safe;
     h.nb = nb;
     h.nb_d = static_cast<double>(nb);
-    const uint64_t rec_bytes = 16ull * (npts + 2);
-    h.off_start = round16(h.off_rec + rec_bytes);
+    h.off_start = round16(h.off_rec + 16ull * (npts + 1));
     h.bytes = round16(h.off_start + 2ull * nb);
-    out.assign(h.bytes, 0);
-    Rec1* R = reinterpret_cast<Rec1*>(out.data() + h.off_rec);
-    R[0] = Rec1{-std::numeric_limits<double>::infinity(), qt::kNoIndex, 0};
-    for (uint64_t s = 0; s < npts; ++s) R[s + 1] = Rec1{v[s], ord[s], 0};
-    R[npts + 1] = Rec1{std::numeric_limits<double>::infinity(), qt::kNoIndex, 0};
-    uint16_t* start = reinterpret_cast<uint16_t*>(out.data() + h.off_start);
-    uint64_t s = 0;
+    out.hot.assign(h.bytes, 0);
+    qt::Thr* T = reinterpret_cast<qt::Thr*>(out.hot.data() + h.off_rec);
+    for (uint64_t c = 0; c < npts; ++c) T[c] = qt::Thr{t[c], ord[c], 0};
+    T[npts] = qt::Thr{std::numeric_limits<double>::infinity(), ord[npts - 1], 0};
+    uint16_t* start = reinterpret_cast<uint16_t*>(out.hot.data() + h.off_start);
+    uint64_t c = 0;
     for (uint32_t b = 0; b < nb; ++b) {
-      while (s < npts && qt::bucket_of(v[s], lo, inv_w, h.nb_d, nb) < b) ++s;
-      start[b] = static_cast<uint16_t>(std::min<uint64_t>(s, 65535));
+      while (c + 1 < npts && qt::bucket_of(t[c], lo, inv_w, h.nb_d, nb) < b) ++c;
+      start[b] = static_cast<uint16_t>(std::min<uint64_t>(c, 65535));
     }
+    out.cold.assign(16ull * npts, 0);
+    Rec1* R = reinterpret_cast<Rec1*>(out.cold.data());
+    for (uint64_t s = 0; s < npts; ++s) R[s] = Rec1{v[s], ord[s], 0};
   } else {
     h.bytes = round16(h.off_rec + 8ull * dim * npts);
-    out.assign(h.bytes, 0);
-    std::memcpy(out.data() + h.off_rec, pts, 8ull * dim * npts);
+    out.hot.assign(h.bytes, 0);
+    std::memcpy(out.hot.data() + h.off_rec, pts, 8ull * dim * npts);
   }
-  std::memcpy(out.data(), &h, sizeof h);
+  std::memcpy(out.hot.data(), &h, sizeof h);
   return out;
 }
 
+void set_cold_off(std::vector<uint8_t>& hot_table, uint64_t cold_off) {
+  LayerTable h;
+  std::memcpy(&h, hot_table.data(), sizeof h);
+  h.cold_off = cold_off;
+  std::memcpy(hot_table.data(), &h, sizeof h);
+}
+
 constexpr uint32_t kMaxTableBytes = 110u * 1024u;  // two must fit in 227 KB of smem
+constexpr uint32_t kStageBudget = 48u * 1024u;     // shared-memory ring per k_paths CTA
 constexpr uint32_t kResidentBudget = 96u * 1024u;
 
 }  // namespace
@@ -395,7 +451,7 @@ struct qt_plan {
   std::vector<uint64_t> sizes, voff, joff;
   uint64_t nvis = 0, njoint = 0, max_cols = 0, max_rows = 0, max_elems = 0;
   std::vector<uint32_t> tab_off, tab_bytes;
-  uint32_t max_tab = 0, total_tab = 0;
+  uint32_t max_tab = 0, total_tab = 0, stages = 2;
   int sm_count = 148;
   uint8_t* d_tables = nullptr;
   uint32_t* d_tab_off = nullptr;
@@ -447,13 +503,16 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
   p->njoint = p->joff[n];
   // tables
   const double* pts = grids->points;
+  std::vector<TableBlob> blobs;
   for (int k = 1; k <= n; ++k) {
     const uint64_t N = p->sizes[k];
     if (N == 0 || N > 0xFFFFFFF0ull)
       raise(QT_ERR_NUMERIC, "grid: point data size is not a positive multiple of dim");
     check_grid(p->dim, N, pts, k);
-    auto t = build_table(p->dim, N, pts, chain->step + 6 * (k - 1), chain->marginal + 6 * (k - 1),
-                         p->joff[k - 1], p->voff[k], p->sizes[k - 1], static_cast<uint32_t>(k));
+    blobs.push_back(build_table(p->dim, N, pts, chain->step + 6 * (k - 1),
+                                chain->marginal + 6 * (k - 1), p->joff[k - 1], p->sizes[k - 1],
+                                static_cast<uint32_t>(k)));
+    const auto& t = blobs.back().hot;
     if (t.size() > kMaxTableBytes)
       raise(QT_ERR_INVALID_ARGUMENT,
             "estimate: layer " + std::to_string(k) + " grid table (" + std::to_string(t.size()) +
@@ -465,6 +524,18 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
     pts += N * p->dim;
   }
   p->total_tab = static_cast<uint32_t>(p->host_tables.size());
+  // cold blocks after all hot tables; patch each header's cold_off
+  for (int k = 1; k <= n; ++k) {
+    TableBlob& b = blobs[k - 1];
+    if (b.cold.empty()) continue;
+    const uint64_t at = p->host_tables.size();
+    std::vector<uint8_t> hot(p->host_tables.begin() + p->tab_off[k - 1],
+                             p->host_tables.begin() + p->tab_off[k - 1] + p->tab_bytes[k - 1]);
+    set_cold_off(hot, at);
+    std::copy(hot.begin(), hot.end(), p->host_tables.begin() + p->tab_off[k - 1]);
+    p->host_tables.insert(p->host_tables.end(), b.cold.begin(), b.cold.end());
+  }
+  p->stages = std::max<uint32_t>(2, std::min<uint32_t>(8, kStageBudget / std::max(p->max_tab, 1u)));
   QT_CUDA(cudaSetDevice(device));
   QT_CUDA(cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, device));
   QT_CUDA(cudaMalloc(&p->d_tables, p->host_tables.size()));
@@ -517,13 +588,15 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
     a.n = static_cast<uint32_t>(p->n);
     a.buf_bytes = p->max_tab;
     a.resident_bytes = p->total_tab;
+    a.stages = p->stages;
+    a.log_stages = 0;
     const bool resident = p->total_tab <= kResidentBudget;
-    const size_t smem = resident ? p->total_tab : 2ull * p->max_tab;
+    const size_t smem = resident ? p->total_tab : static_cast<size_t>(p->stages) * p->max_tab;
     const int bps = qt::paths_blocks_per_sm(p->kind, src, resident, smem);
     uint64_t blocks = static_cast<uint64_t>(p->sm_count) * bps;
-    const uint64_t need = (count + 255) / 256;
+    const uint64_t need = (count + qt::kPathConsumers - 1) / qt::kPathConsumers;
     if (need < blocks) blocks = need;
-    const uint64_t T = blocks * 256;
+    const uint64_t T = blocks * qt::kPathConsumers;
     a.q = count / T;
     a.rem = count % T;
     QT_CUDA(qt::launch_paths(p->kind, src, resident, a, static_cast<uint32_t>(blocks), smem, st));
@@ -871,7 +944,11 @@ QT_API qt_status qt_nearest(int32_t dim, uint64_t n_points, const double* points
     if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
       raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
     double zeros[6] = {0, 0, 0, 0, 0, 0};
-    auto t = build_table(dim, n_points, points, zeros, zeros, 0, 0, 1, 1);
+    TableBlob tb = build_table(dim, n_points, points, zeros, zeros, 0, 1, 1);
+    std::vector<uint8_t> t = tb.hot;
+    const uint32_t hot_bytes = static_cast<uint32_t>(t.size());
+    set_cold_off(t, t.size());
+    t.insert(t.end(), tb.cold.begin(), tb.cold.end());
     QT_CUDA(cudaSetDevice(0));
     uint8_t* d_t = nullptr;
     double* d_q = nullptr;
@@ -887,8 +964,7 @@ QT_API qt_status qt_nearest(int32_t dim, uint64_t n_points, const double* points
       QT_CUDA(cudaMalloc(&d_o, n_queries * sizeof(uint64_t)));
       QT_CUDA(cudaMemcpy(d_t, t.data(), t.size(), cudaMemcpyHostToDevice));
       QT_CUDA(cudaMemcpy(d_q, queries, n_queries * dim * sizeof(double), cudaMemcpyHostToDevice));
-      QT_CUDA(qt::launch_nearest(dim, d_t, static_cast<uint32_t>(t.size()), d_q, n_queries, d_o,
-                                 nullptr));
+      QT_CUDA(qt::launch_nearest(dim, d_t, hot_bytes, d_q, n_queries, d_o, nullptr));
       g_launches.fetch_add(1);
       QT_CUDA(cudaMemcpy(out, d_o, n_queries * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     } catch (...) {

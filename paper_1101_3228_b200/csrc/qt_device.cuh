@@ -375,47 +375,45 @@ struct Chain<3> {  // GBM 3-D basket log-state
 // reference's d2, smallest original index on ties.
 // ---------------------------------------------------------------------------
 
-// Exact scan over the sorted records with (d2, original index) ordering:
-// identical result to the reference's ascending strict-< scan for every x.
+// Exact scan over the sorted records (cold block, global memory) with
+// (d2, original index) ordering: identical result to the reference's
+// ascending strict-< scan for every x, including NaN / +-inf / overflow.
 __device__ __noinline__ uint32_t nearest_1d_scan(const Rec1* R, uint32_t n, double x) {
   uint32_t best = 0;
   double bd = __longlong_as_double(0x7ff0000000000000ll);  // +inf
-  for (uint32_t s = 1; s <= n; ++s) {
-    const double d = __dsub_rn(x, R[s].v);
+  for (uint32_t s = 0; s < n; ++s) {
+    const Rec1 r = R[s];
+    const double d = __dsub_rn(x, r.v);
     const double d2 = __dmul_rn(d, d);
-    if (d2 < bd || (d2 == bd && R[s].orig < best)) {
+    if (d2 < bd || (d2 == bd && r.orig < best)) {
       bd = d2;
-      best = R[s].orig;
+      best = r.orig;
     }
   }
   return best;
 }
 
-// d == 1: bucket jump into the sorted records, bracket, compare the two
-// neighbours. Exact whenever |x| < x_safe (no same-side ties possible, see
-// DESIGN.md "1-D projection"); otherwise (or for NaN/inf) the exact scan.
-__device__ __forceinline__ uint32_t nearest_1d(const LayerTable& h, const uint8_t* base, double x) {
-  const Rec1* R = reinterpret_cast<const Rec1*>(base + h.off_rec);
-  if (!(fabs(x) < h.x_safe)) return nearest_1d_scan(R, h.n_pts, x);
+// d == 1. The reference's argmin of fl(fl(x - v)^2) over a sorted grid is
+// decided by the two values bracketing x, and that pairwise choice (with the
+// smallest-index tie rule) flips exactly once on [v_c, v_c+1]: at the FP64
+// decision threshold t_c the host finds by bisection over the doubles. So the
+// cell is the number of thresholds <= x: one bucket lookup, one 16-byte
+// shared-memory record pair, two FP64 compares. Exact whenever |x| < x_safe
+// (no same-side d2 ties possible); otherwise (and for NaN/inf)
+// the exact scan over the cold block.
+__device__ __forceinline__ uint32_t nearest_1d(const LayerTable& h, const uint8_t* base, double x,
+                                               const uint8_t* gtables) {
+  if (!(fabs(x) < h.x_safe))
+    return nearest_1d_scan(reinterpret_cast<const Rec1*>(gtables + h.cold_off), h.n_pts, x);
+  const Thr* T = reinterpret_cast<const Thr*>(base + h.off_rec);
   const uint16_t* start = reinterpret_cast<const uint16_t*>(base + h.off_start);
-  const uint32_t b = bucket_of(x, h.lo, h.inv_w, h.nb_d, h.nb);
-  uint32_t s = start[b];  // R[s] = sorted point s-1 < x (or -inf sentinel)
-  Rec1 lo = R[s], hi = R[s + 1];
-  if (!(x < hi.v)) {
-    lo = hi;
-    hi = R[s + 2];
-    if (!(x < hi.v)) {
-      s += 2;
-      while (!(x < R[s + 1].v)) ++s;
-      lo = R[s];
-      hi = R[s + 1];
-    }
-  }
-  const double dl = __dsub_rn(x, lo.v);
-  const double dh = __dsub_rn(x, hi.v);
-  const double d2l = __dmul_rn(dl, dl);
-  const double d2h = __dmul_rn(dh, dh);
-  return d2l < d2h ? lo.orig : (d2h < d2l ? hi.orig : min(lo.orig, hi.orig));
+  uint32_t c = start[bucket_of(x, h.lo, h.inv_w, h.nb_d, h.nb)];  // all t_{<c} < x
+  const Thr r0 = T[c], r1 = T[c + 1];
+  if (x < r0.t) return r0.orig;
+  if (x < r1.t) return r1.orig;
+  c += 2;
+  while (!(x < T[c].t)) ++c;  // t_{N-1} = +inf stops the walk
+  return T[c].orig;
 }
 
 // d == 2: the reference's fast path dx*dx + dy*dy (nn.hpp:25-37), strict <.
@@ -463,8 +461,8 @@ __device__ __forceinline__ uint32_t nearest_3d(const LayerTable& h, const uint8_
 
 template <int D>
 __device__ __forceinline__ uint32_t nearest(const LayerTable& h, const uint8_t* base,
-                                            const double* q) {
-  if constexpr (D == 1) return nearest_1d(h, base, q[0]);
+                                            const double* q, const uint8_t* gtables) {
+  if constexpr (D == 1) return nearest_1d(h, base, q[0], gtables);
   else if constexpr (D == 2) return nearest_2d(h, base, q);
   else return nearest_3d(h, base, q);
 }

@@ -34,7 +34,11 @@ struct PathArgs {
   uint32_t n;
   uint32_t buf_bytes;         // staging buffer size (max table bytes)
   uint32_t resident_bytes;    // sum of table bytes (resident mode)
+  uint32_t stages;            // shared-memory ring depth (power of 2, <= 8)
+  uint32_t log_stages;
 };
+
+constexpr int kPathConsumers = 256;  // consumer threads per k_paths CTA
 
 struct Alg3Args {
   SrcArgs src;

@@ -2,11 +2,12 @@
 //
 //  k_paths   K1+K2+K3 fused: Alg I/II path kernel (estimate.hpp:88-126). One
 //            thread owns a contiguous run of paths (so its MRG32k3a state
-//            flows from path to path without jumps), the CTA walks the layers
-//            in lock-step and double-buffers each layer's grid table into
-//            shared memory with cp.async.bulk + mbarrier; each transition is
-//            normals -> chain step -> exact Voronoi projection -> one
-//            red.global.add.u64 into joint[k-1][i*N_k + j].
+//            flows from path to path without jumps). A producer warp streams
+//            each layer's grid table into a ring of shared-memory stages with
+//            cp.async.bulk (full/empty mbarriers); eight consumer warps do, per
+//            transition, normals -> chain step -> exact Voronoi projection
+//            (one FP64 threshold record pair) -> one red.global.add.u64 into
+//            joint[k-1][i*N_k + j].
 //  k_alg3    K4: Alg III layer-parallel pair sampler (estimate.hpp:213-265):
 //            CTA = (layer k, slice of its M samples), tables of layers k-1 and
 //            k resident in shared memory, two projections per sample.
@@ -24,50 +25,75 @@ namespace qt {
 constexpr int kThreads = 256;
 
 // ---------------------------------------------------------------------------
-// Alg I / II
+// Alg I / II. Warp-specialised: warp 8 is the TMA producer, warps 0-7 the
+// consumers. Layer tables cycle through S shared-memory stages guarded by a
+// full/empty mbarrier ring, so consumer warps never meet at a CTA barrier and
+// may drift up to S layers apart.
 // ---------------------------------------------------------------------------
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kPathThreads = kConsumers + 32;
+constexpr int kMaxStages = 8;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 template <int K, int SRC, bool RESIDENT>
-__global__ void __launch_bounds__(kThreads) k_paths(const PathArgs a) {
+__global__ void __launch_bounds__(kPathThreads) k_paths(const PathArgs a) {
   using C = Chain<K>;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bars[2];
-  const uint32_t tid = threadIdx.x;
-  const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + tid;
-  const uint64_t mycount = a.q + (g < a.rem ? 1u : 0u);
-  const uint64_t mybeg = a.first + g * a.q + (g < a.rem ? g : a.rem);
+  __shared__ __align__(8) uint64_t full[kMaxStages];
+  __shared__ __align__(8) uint64_t empty[kMaxStages];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+  const uint32_t S = a.stages;
   const uint64_t rounds = a.q + (a.rem ? 1u : 0u);
   const uint64_t steps_total = rounds * a.n;
   if (steps_total == 0) return;
 
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (uint32_t s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if constexpr (RESIDENT) {
-    // Every layer table fits: stage them all once, no per-layer barrier.
-    if (tid == 0) {
-      mbar_expect_tx(&bars[0], a.resident_bytes);
-      for (uint32_t k = 0; k < a.n; ++k)
-        bulk_g2s(smem + (a.tab_off[k] - a.tab_off[0]), a.tables + a.tab_off[k], a.tab_bytes[k],
-                 &bars[0]);
-    }
-    mbar_wait(&bars[0], 0);
-  } else {
-    if (tid == 0) {
-      for (uint32_t s = 0; s < 2 && s < steps_total; ++s) {
-        const uint32_t k = static_cast<uint32_t>(s % a.n);
-        mbar_expect_tx(&bars[s], a.tab_bytes[k]);
-        bulk_g2s(smem + s * a.buf_bytes, a.tables + a.tab_off[k], a.tab_bytes[k], &bars[s]);
+  if (warp == kConsumerWarps) {  // ---- producer warp ----
+    if (lane == 0) {
+      if constexpr (RESIDENT) {
+        mbar_expect_tx(&full[0], a.resident_bytes);
+        for (uint32_t k = 0; k < a.n; ++k)
+          bulk_g2s(smem + (a.tab_off[k] - a.tab_off[0]), a.tables + a.tab_off[k], a.tab_bytes[k],
+                   &full[0]);
+      } else {
+        uint32_t k = 0, s = 0, ph = 0;
+        for (uint64_t g = 0; g < steps_total; ++g) {
+          mbar_wait(&empty[s], ph ^ 1u);  // a fresh barrier passes parity 1 at once
+          const uint32_t bytes = __ldg(a.tab_bytes + k);
+          mbar_expect_tx(&full[s], bytes);
+          bulk_g2s(smem + s * a.buf_bytes, a.tables + __ldg(a.tab_off + k), bytes, &full[s]);
+          k = k + 1 == a.n ? 0 : k + 1;
+          if (++s == S) {
+            s = 0;
+            ph ^= 1u;
+          }
+        }
       }
     }
+    return;
   }
+
+  // ---- consumer warps: one path at a time per thread ----
+  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * kConsumers + tid;
+  const uint64_t mycount = a.q + (gid < a.rem ? 1u : 0u);
+  const uint64_t mybeg = a.first + gid * a.q + (gid < a.rem ? gid : a.rem);
+  if constexpr (RESIDENT) mbar_wait(&full[0], 0);
 
   Source<SRC> src;
   if (mycount) src.start(a.src, mybeg);
-  uint64_t step_no = 0;
+  uint32_t s = 0, ph = 0;  // ring position
   for (uint64_t r = 0; r < rounds; ++r) {
     const bool active = r < mycount;
     if (active && r > 0) src.next_unit(a.src, mybeg + r);
@@ -75,14 +101,13 @@ __global__ void __launch_bounds__(kThreads) k_paths(const PathArgs a) {
 #pragma unroll
     for (int d = 0; d < C::D; ++d) x[d] = 0.0;  // initial(): the origin (chains.hpp:43-46,81)
     uint32_t i = 0;                             // layer 0 is the singleton {x0}
-    for (uint32_t k = 1; k <= a.n; ++k, ++step_no) {
+    for (uint32_t k = 1; k <= a.n; ++k) {
       const uint8_t* tb;
       if constexpr (RESIDENT) {
         tb = smem + (a.tab_off[k - 1] - a.tab_off[0]);
       } else {
-        const uint32_t b = static_cast<uint32_t>(step_no & 1u);
-        tb = smem + b * a.buf_bytes;
-        mbar_wait(&bars[b], static_cast<uint32_t>((step_no >> 1) & 1u));
+        tb = smem + s * a.buf_bytes;
+        mbar_wait(&full[s], ph);
       }
       const LayerTable& h = *reinterpret_cast<const LayerTable*>(tb);
       if (active) {
@@ -92,20 +117,16 @@ __global__ void __launch_bounds__(kThreads) k_paths(const PathArgs a) {
         C::step(h.step, x, xn, e);
 #pragma unroll
         for (int d = 0; d < C::D; ++d) x[d] = xn[d];
-        const uint32_t j = nearest<C::D>(h, tb, x);
+        const uint32_t j = nearest<C::D>(h, tb, x, a.tables);
         red_add_u64(a.joint + h.joff + static_cast<uint64_t>(i) * h.n_pts + j, 1ull);
         i = j;
       }
       if constexpr (!RESIDENT) {
-        __syncthreads();  // every thread is done with this buffer
-        if (tid == 0) {
-          const uint64_t s2 = step_no + 2;
-          if (s2 < steps_total) {
-            const uint32_t b = static_cast<uint32_t>(step_no & 1u);
-            const uint32_t kk = static_cast<uint32_t>(s2 % a.n);
-            mbar_expect_tx(&bars[b], a.tab_bytes[kk]);
-            bulk_g2s(smem + b * a.buf_bytes, a.tables + a.tab_off[kk], a.tab_bytes[kk], &bars[b]);
-          }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == S) {
+          s = 0;
+          ph ^= 1u;
         }
       }
     }
@@ -161,8 +182,8 @@ __global__ void __launch_bounds__(kThreads) k_alg3(const Alg3Args a) {
     for (int q2 = 0; q2 < C::D + C::NPS; ++q2) e[q2] = src.normal();
     C::marginal(hk.marg_prev, k == 1, x, e);  // sample_marginal(k-1, ...)
     C::step(hk.step, x, xn, e + C::D);        // step(k-1, ...)
-    const uint32_t i = k == 1 ? 0u : nearest<C::D>(hp, tp, x);
-    const uint32_t j = nearest<C::D>(hk, tk, xn);
+    const uint32_t i = k == 1 ? 0u : nearest<C::D>(hp, tp, x, a.tables);
+    const uint32_t j = nearest<C::D>(hk, tk, xn, a.tables);
     red_add_u64(a.joint + hk.joff + static_cast<uint64_t>(i) * hk.n_pts + j, 1ull);
   }
 }
@@ -249,7 +270,7 @@ __global__ void __launch_bounds__(kThreads) k_nearest(const uint8_t* table, uint
     double x[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) x[d] = queries[q * D + d];
-    out[q] = nearest<D>(h, tb, x);
+    out[q] = nearest<D>(h, tb, x, table);
   }
 }
 
@@ -282,7 +303,7 @@ static cudaError_t launch_paths_t(const PathArgs& a, dim3 grid, size_t smem, cud
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  fn<<<grid, kThreads, smem, st>>>(a);
+  fn<<<grid, kPathThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -337,7 +358,7 @@ int paths_blocks_per_sm(int kind, int src, bool resident, size_t smem) {
 #undef QT_PICK
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kPathThreads, smem) != cudaSuccess)
     return 1;
   return nb > 0 ? nb : 1;
 }

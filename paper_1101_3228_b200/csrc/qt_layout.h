@@ -1,14 +1,19 @@
 // qt_layout.h -- host/device shared layout of the per-layer "grid tables"
 // that the path kernels stage into shared memory with cp.async.bulk.
 //
-// One table per layer k = 1..n, 16-byte aligned, contiguous in HBM:
+// One table per layer k = 1..n, 16-byte aligned, contiguous in HBM ("hot"
+// part, staged into shared memory):
 //
 //   LayerTable header (192 B)
-//   d == 1 : Rec1[N + 2]       sorted points {value, original index}, with
-//                              -inf / +inf sentinels at [0] and [N + 1]
-//            uint16 start[nb]  bucket -> first sorted position whose bucket >= b
+//   d == 1 : Thr[N + 1]        per sorted cell c: {t_c, original index of c};
+//                              t_c is the exact FP64 decision threshold between
+//                              sorted cells c and c+1 (t_{N-1} = t_N = +inf)
+//            uint16 start[nb]  bucket b -> #{thresholds whose bucket < b}
 //   d >= 2 : double pts[N * d] points in ORIGINAL order (row-major), the
 //                              reference's scan order (nn.hpp:25-45)
+//
+// plus, for d == 1, a "cold" block (never staged, read from global memory by
+// the exact fallback scan only): Rec1[N] sorted {value, original index}.
 //
 // The header also carries the chain coefficients of the transition that lands
 // on this layer (step of k-1 -> k) and the marginal factor of layer k-1, so a
@@ -19,25 +24,32 @@
 namespace qt {
 
 struct alignas(16) LayerTable {
-  double lo;            // d == 1: smallest grid value (bucket origin)
+  double lo;            // d == 1: bucket origin (smallest threshold)
   double inv_w;         // d == 1: buckets per unit of x
-  double x_safe;        // d == 1: |x| < x_safe => no same-side d2 ties (fast path exact)
+  double x_safe;        // d == 1: |x| < x_safe => threshold rule is exact
   double nb_d;          // (double)nb
   double step[6];       // chain coefficients of transition k-1 -> k
   double marg_prev[6];  // marginal factor of layer k-1 (Alg III)
   uint64_t joff;        // element offset of joint[k-1] in the flat joint array
-  uint64_t voff;        // element offset of visits[k]
+  uint64_t cold_off;    // d == 1: byte offset (from the tables base) of Rec1[N]
   uint32_t n_pts;       // N_k
   uint32_t n_prev;      // N_{k-1}
   uint32_t nb;          // d == 1: number of buckets
-  uint32_t off_rec;     // byte offset of Rec1[] / pts[] from the table start
+  uint32_t off_rec;     // byte offset of Thr[] / pts[] from the table start
   uint32_t off_start;   // byte offset of start[] (d == 1)
-  uint32_t bytes;       // total table bytes (multiple of 16)
+  uint32_t bytes;       // hot table bytes (multiple of 16)
   uint32_t layer;       // k
   uint32_t dim;
   uint32_t pad_[4];
 };
 static_assert(sizeof(LayerTable) == 192, "LayerTable header is 192 bytes");
+
+struct alignas(16) Thr {
+  double t;
+  uint32_t orig;
+  uint32_t pad;
+};
+static_assert(sizeof(Thr) == 16, "Thr is 16 bytes");
 
 struct alignas(16) Rec1 {
   double v;
