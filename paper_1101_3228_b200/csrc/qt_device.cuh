@@ -13,6 +13,7 @@
 
 #include "qt_internal.h"
 #include "qt_layout.h"
+#include "qt_math.h"
 
 namespace qt {
 
@@ -182,17 +183,19 @@ __device__ __forceinline__ Xorwow xorwow_stream(uint64_t seed, uint64_t stream) 
 // ---------------------------------------------------------------------------
 // Box-Muller (stream.hpp:57-62): r = sqrt(-2 log u1), a = 2 pi u2,
 // (r cos a, r sin a); u1 <= 0 clamps to 2^-64. sqrt and the products are
-// correctly rounded like glibc's; log/sin/cos are CUDA's (<= 1-2 ulp), the
-// one documented non-bit-identical step (normals-in mode is exact).
+// correctly rounded like glibc's; log and sin/cos are the domain-specialised
+// kernels of qt_math.h (<= 1 ulp; 99.8 % / 96.9 % bit-identical to glibc,
+// tests/test_math_kernels.py) -- the one step that is not bit-identical by
+// construction (normals-in mode is exact).
 // ---------------------------------------------------------------------------
 constexpr double kTwoPi = 6.283185307179586;  // 2.0 * std::numbers::pi, exact doubling
 
 __device__ __forceinline__ void box_muller(double u1, double u2, double& z1, double& z2) {
   if (u1 <= 0.0) u1 = 0x1p-64;
-  const double r = __dsqrt_rn(__dmul_rn(-2.0, log(u1)));
+  const double r = __dsqrt_rn(__dmul_rn(-2.0, qt_log_unit(u1)));
   const double a = __dmul_rn(kTwoPi, u2);
   double s, c;
-  sincos(a, &s, &c);
+  qt_sincos_2pi(a, &s, &c);
   z1 = __dmul_rn(r, c);
   z2 = __dmul_rn(r, s);
 }
@@ -496,10 +499,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(0x100000u)  // suspend (not spin) up to ~1 ms
         : "memory");
   } while (!done);
 }
