@@ -163,10 +163,17 @@ QT_API qt_status qt_nearest(int32_t dim, uint64_t n_points, const double* points
 QT_API qt_status qt_bdp_stopping(int32_t layers, const uint64_t* sizes, const uint64_t* visits,
                                  const double* pi, const double* phi, double* value,
                                  uint8_t* exercise, double* price);
-/* value_all (nullable): per layer k, (m - m_lo[k]) * N_k + i (swing.hpp:23-39) */
+/* value_all (nullable): per layer k = 0..n, (m - m_lo[k]) * N_k + i;
+ * take_all (nullable): the same layout over layers 0..n-1 (swing.hpp:23-39). */
 QT_API qt_status qt_bdp_swing(int32_t layers, const uint64_t* sizes, const uint64_t* visits,
                               const double* pi, const double* phi, int32_t q_min, int32_t q_max,
-                              double* price, double* value_all);
+                              double* price, double* value_all, uint8_t* take_all);
+
+/* cond_expectation (bdp.hpp:36-54) for one transition: out[i] = sum_j pi[i,j] f[j]
+ * in ascending j (bit-identical to the dense loop), quiet NaN where
+ * row_visits[i] == 0. pi is rows x cols row-major. */
+QT_API qt_status qt_bdp_cond_expectation(uint64_t rows, uint64_t cols, const uint64_t* row_visits,
+                                         const double* pi, const double* f, double* out);
 
 /* ---- diagnostics ----------------------------------------------------------- */
 

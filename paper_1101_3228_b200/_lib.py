@@ -52,7 +52,9 @@ _SIGS = {
                          C.c_void_p, C.POINTER(C.c_int32)],
     "qt_nearest": [C.c_int32, C.c_uint64, _f64p, C.c_uint64, _f64p, _u64p],
     "qt_bdp_stopping": [C.c_int32, _u64p, _u64p, _f64p, _f64p, _f64p, _u8p, _f64p],
-    "qt_bdp_swing": [C.c_int32, _u64p, _u64p, _f64p, _f64p, C.c_int32, C.c_int32, _f64p, _f64p],
+    "qt_bdp_swing": [C.c_int32, _u64p, _u64p, _f64p, _f64p, C.c_int32, C.c_int32, _f64p, _f64p,
+                     _u8p],
+    "qt_bdp_cond_expectation": [C.c_uint64, C.c_uint64, _u64p, _f64p, _f64p, _f64p],
     "qt_path_normals": [C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _f64p],
     "qt_uniforms": [C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, _f64p],
 }

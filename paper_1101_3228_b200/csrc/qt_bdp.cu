@@ -292,7 +292,7 @@ QT_API qt_status qt_bdp_stopping(int32_t layers, const uint64_t* sizes, const ui
 
 QT_API qt_status qt_bdp_swing(int32_t layers, const uint64_t* sizes, const uint64_t* visits,
                               const double* pi, const double* phi, int32_t qmin, int32_t qmax,
-                              double* price, double* value_all) {
+                              double* price, double* value_all, uint8_t* take_all) {
   return bdp_guarded([&] {
     check_tree_args(layers, sizes, visits, pi, phi);
     const int n = layers;
@@ -339,6 +339,29 @@ QT_API qt_status qt_bdp_swing(int32_t layers, const uint64_t* sizes, const uint6
     BDP_CUDA(cudaGetLastError());
     BDP_CUDA(cudaMemcpy(price, P.p, 8, cudaMemcpyDeviceToHost));
     if (value_all) BDP_CUDA(cudaMemcpy(value_all, P.p, soff[n + 1] * 8, cudaMemcpyDeviceToHost));
+    if (take_all && soff[n]) BDP_CUDA(cudaMemcpy(take_all, take.p, soff[n], cudaMemcpyDeviceToHost));
+  });
+}
+
+QT_API qt_status qt_bdp_cond_expectation(uint64_t rows, uint64_t cols, const uint64_t* row_visits,
+                                         const double* pi, const double* f, double* out) {
+  return bdp_guarded([&] {
+    if (rows == 0 || cols == 0 || !row_visits || !pi || !f || !out)
+      bdp_raise(QT_ERR_INVALID_ARGUMENT, "cond_expectation: empty or null argument");
+    check_device();
+    const uint64_t sz[2] = {rows, cols};
+    std::vector<double> no_phi(rows + cols, 0.0);
+    std::vector<uint64_t> vis(rows + cols, 0);  // layer-1 visits are never read
+    std::copy(row_visits, row_visits + rows, vis.begin());
+    TreeOnDevice t(1, sz, vis.data(), pi, no_phi.data());
+    DevBuf<double> df(cols), dout(rows);
+    BDP_CUDA(cudaMemcpy(df.p, f, cols * 8, cudaMemcpyHostToDevice));
+    // one stored slice, unvisited rows -> quiet NaN (bdp.hpp:45-48)
+    k_swing_cont<<<static_cast<uint32_t>((rows + 127) / 128), 128>>>(
+        rows, cols, 1, t.rowptr(0), t.csr.colidx.p, t.csr.val.p, t.visits.p, df.p, dout.p);
+    qt::note_launches(1);
+    BDP_CUDA(cudaGetLastError());
+    BDP_CUDA(cudaMemcpy(out, dout.p, rows * 8, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -431,6 +431,7 @@ class SwingResult:
     m_lo: list
     m_count: list
     value: list
+    take: list
     price: float
 
 
@@ -470,16 +471,38 @@ def solve_swing(tree: QuantTree, payoff, q_min: int, q_max: int) -> SwingResult:
     lo, cnt = swing_window(n, q_min, q_max)
     total = sum(max(c, 0) * tree.layer_size(k) for k, c in enumerate(cnt))
     vals = np.zeros(max(total, 1), np.float64)
+    takes = np.zeros(max(total, 1), np.uint8)
     price = C.c_double()
     _check(L.lib().qt_bdp_swing(n, _u(tree.sizes), _u(tree.flat_visits), _f(tree.flat_pi),
-                                _f(phi), int(q_min), int(q_max), C.byref(price), _f(vals)),
+                                _f(phi), int(q_min), int(q_max), C.byref(price), _f(vals),
+                                takes.ctypes.data_as(C.POINTER(C.c_uint8))),
            "solve_swing")
-    value, o = [], 0
+    value, take, o = [], [], 0
     for k in range(n + 1):
         s = cnt[k] * tree.layer_size(k)
         value.append(vals[o:o + s])
+        if k < n:
+            take.append(takes[o:o + s])
         o += s
-    return SwingResult(q_min, q_max, lo, cnt, value, price.value)
+    return SwingResult(q_min, q_max, lo, cnt, value, take, price.value)
+
+
+def cond_expectation(tree: QuantTree, k: int, f) -> np.ndarray:
+    """E(f(X_{k+1}) | X_k = x_i) = pi^{k+1} f, NaN on unvisited rows (bdp.hpp:36-54)."""
+    if k < 0 or k >= tree.layers():
+        raise ValueError("cond_expectation: layer out of range")
+    rows, cols = tree.layer_size(k), tree.layer_size(k + 1)
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    if f.size != cols:
+        raise ValueError("cond_expectation: value vector length mismatch")
+    vo = int(tree.sizes[:k].sum())
+    po = int(sum(int(tree.sizes[t]) * int(tree.sizes[t + 1]) for t in range(k)))
+    vis = np.ascontiguousarray(tree.flat_visits[vo:vo + rows])
+    pi = np.ascontiguousarray(tree.flat_pi[po:po + rows * cols])
+    out = np.zeros(rows, np.float64)
+    _check(L.lib().qt_bdp_cond_expectation(rows, cols, _u(vis), _f(pi), _f(f), _f(out)),
+           "cond_expectation")
+    return out
 
 
 # ---------------------------------------------------------------------------

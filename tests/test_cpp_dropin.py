@@ -1,0 +1,65 @@
+"""The C++ drop-in headers (include/qtree/...) as a reference user compiles
+them: this repo's include/ first, the reference's after it, libqtree_cuda.so
+linked. tests/cpp/Makefile builds (in this container, where /root/reference
+exists) the reference's own UNMODIFIED test_tree.cpp / test_pricer.cpp on a
+Catch2 shim, plus test_dropin.cpp (checks against oracle/_ref). The binaries
+travel to the GPU box; the -m gpu tests run them there."""
+from __future__ import annotations
+
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "tests", "cpp", "_bin")
+PROGRAMS = ["ref_test_tree", "ref_test_pricer", "test_dropin"]
+
+# Sections of the reference's tests that are undefined behaviour in the
+# reference itself and therefore cannot be judged: test_pricer.cpp:307-310
+# loops i < 3 over every layer, but layer 0 has one node, so it reads
+# cond_expectation(...)[1] and exercise[0][1] past the end of 1-element
+# vectors (AddressSanitizer: heap-buffer-overflow at test_pricer.cpp:309 when
+# built against the reference's own headers). What the garbage compares to
+# depends on the heap, not on the pricer.
+KNOWN_UB_SECTIONS = ["price report/stopping frontier marks exactly payoff >= continuation"]
+
+
+def _binary(name):
+    path = os.path.join(BIN, name)
+    if not os.path.exists(path):
+        if os.path.isdir("/root/reference/proj"):
+            subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+        else:
+            pytest.fail(f"{path} missing: run __graft_entry__.build() where /root/reference exists")
+    return path
+
+
+def test_dropin_headers_compile_against_reference_callers():
+    if not os.path.isdir("/root/reference/proj"):
+        pytest.skip("compile-time check needs the reference tree")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    for p in PROGRAMS:
+        assert os.path.exists(os.path.join(BIN, p)), p
+
+
+def test_dropin_has_no_cpu_fallback_in_cpp():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("checks the no-device path")
+    out = subprocess.run([_binary("test_dropin"), "errors"], capture_output=True, text=True,
+                         cwd=ROOT, timeout=120)
+    # the device entry refuses to run: NumericError("cuda: ...") surfaces in C++
+    assert "cuda: no CUDA device available" in out.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("program", PROGRAMS)
+def test_cpp_program_passes_on_device(gpu, program):
+    env = dict(os.environ, CATCH_SHIM_SKIP=";".join(KNOWN_UB_SECTIONS))
+    out = subprocess.run([_binary(program)], capture_output=True, text=True, cwd=ROOT, timeout=900,
+                         env=env)
+    print(out.stdout[-4000:])
+    print(out.stderr[-4000:])
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert " 0 failures" in out.stdout
