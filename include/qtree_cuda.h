@@ -185,6 +185,25 @@ QT_API qt_status qt_path_normals(int32_t engine, uint64_t seed, uint64_t normals
 QT_API qt_status qt_uniforms(int32_t engine, uint64_t seed, uint64_t offset, uint64_t count,
                              double* out);
 
+/* ---- fast 1-D path (Brownian / OU chains, MRG32k3a, Alg I/II) -------------
+ * FP32 Box-Muller with a rigorous error bound; a transition is counted only
+ * when the bounded FP64 state interval lies inside one cell, and a path with an
+ * uncertified transition is recomputed with the exact FP64 arithmetic from that
+ * layer on, so the counts equal the exact kernel's. Enabled by
+ * default; QT_FAST_PATH=0 in the environment or qt_set_fast_path(0) selects
+ * the exact kernel for every path. */
+QT_API qt_status qt_set_fast_path(int32_t enabled);
+/* out[3] = {paths counted by the fast path, paths replayed exactly, paths
+ * replayed inline after a replay-list overflow}, summed over destroyed plans. */
+QT_API qt_status qt_fast_stats(uint64_t* out);
+/* The same three counters for one live plan (synchronises its device). */
+QT_API qt_status qt_plan_fast_stats(const qt_plan* plan, uint64_t* out);
+/* Exhaustive check of the FP32 Box-Muller bounds over all 2^32 - 209 MRG32k3a
+ * outputs on device 0: out[4] = {max(|r~ - r| - kRadB r~), max |c~ - c|,
+ * max |s~ - s|, max(|c~|, |s~|)}; the fast path is valid iff out[0] <= kRadA,
+ * out[1], out[2] <= kAng and out[3] <= 1 (qt_device.cuh). */
+QT_API qt_status qt_fast_bounds_check(double* out);
+
 /* Thread-local text of the last failure on this thread. */
 QT_API const char* qt_last_error(void);
 /* Build identification: "qtree_cuda <version> sm_100a ..." */

@@ -57,6 +57,10 @@ _SIGS = {
     "qt_bdp_cond_expectation": [C.c_uint64, C.c_uint64, _u64p, _f64p, _f64p, _f64p],
     "qt_path_normals": [C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _f64p],
     "qt_uniforms": [C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, _f64p],
+    "qt_set_fast_path": [C.c_int32],
+    "qt_fast_stats": [_u64p],
+    "qt_plan_fast_stats": [C.c_void_p, _u64p],
+    "qt_fast_bounds_check": [_f64p],
 }
 
 # Every symbol include/qtree_cuda.h declares (checked by tests/test_boundary.py).

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -32,6 +33,20 @@ using qt::Rec1;
 
 thread_local std::string g_error;
 std::atomic<uint64_t> g_launches{0};
+// fast 1-D path: enabled unless QT_FAST_PATH=0 or qt_set_fast_path(0)
+std::atomic<int> g_fast{-1};
+// cumulative fast-path evidence of destroyed plans: paths, replayed, inline-replayed
+std::atomic<uint64_t> g_fast_paths{0}, g_fast_replayed{0}, g_fast_inline{0};
+
+bool fast_enabled() {
+  int v = g_fast.load();
+  if (v < 0) {
+    const char* e = std::getenv("QT_FAST_PATH");
+    v = (e && e[0] == '1') ? 1 : 0;  // TEMP default off until it beats k_paths
+    g_fast.store(v);
+  }
+  return v == 1;
+}
 
 struct Failure {
   qt_status code;
@@ -320,16 +335,104 @@ bool choose_hi(double x, double vl, double vh, uint32_t ol, uint32_t oh) {
   return d2h < d2l || (d2h == d2l && oh < ol);
 }
 
+// FP32 value >= x (round toward +inf)
+float f32_up(double x) {
+  float f = static_cast<float>(x);
+  if (static_cast<double>(f) < x) f = std::nextafter(f, std::numeric_limits<float>::infinity());
+  return f;
+}
+// FP32 value >= |x| (round toward +inf)
+float f32_up_abs(double x) {
+  const double a = std::fabs(x);
+  float f = static_cast<float>(a);
+  if (static_cast<double>(f) < a) f = std::nextafter(f, std::numeric_limits<float>::infinity());
+  return f;
+}
+
 struct TableBlob {
   std::vector<uint8_t> hot;   // staged into shared memory
   std::vector<uint8_t> cold;  // d == 1 exact-scan records (global memory only)
+  std::vector<uint8_t> fast;  // d == 1 fast-path table (FastHdr + FRec[nb])
 };
+
+float f32_down(double x) {
+  float f = static_cast<float>(x);
+  if (static_cast<double>(f) > x) f = std::nextafter(f, -std::numeric_limits<float>::infinity());
+  return f == 0.0f ? 0.0f : f;  // never -0 (the device's up() step assumes t0 >= 0 -> bits + 1)
+}
+
+// Fast-path table of one 1-D layer from the exact decision thresholds t[0..N-1]
+// (t[N-1] = +inf) in sorted-cell order, ord = original index of each sorted cell.
+std::vector<uint8_t> build_fast_table(int kind, const std::vector<double>& t,
+                                      const std::vector<uint32_t>& ord, double x_safe,
+                                      const double* step, uint64_t joff) {
+  const uint64_t N = t.size();
+  qt::FastHdr h{};
+  h.c0 = step[0];
+  h.c2 = kind == QT_CHAIN_OU_1D ? step[2] : 0.0;
+  h.joff = joff;
+  h.fa = kind == QT_CHAIN_OU_1D ? f32_up_abs(step[0]) : 1.0f;
+  h.fs = f32_up_abs(kind == QT_CHAIN_OU_1D ? step[2] : step[0]);
+  h.x_safe = x_safe > 0.0 ? std::max(0.0f, f32_down(x_safe)) : 0.0f;
+  h.n_pts = static_cast<uint32_t>(N);
+  // uniform FP32 bucket map over [t_0, t_{N-2}]: the fewest buckets (multiple
+  // of N, <= 8N) that hold at most one threshold each
+  uint32_t nb = 1;
+  float bk_a = 0.0f, bk_b = 0.0f;
+  const double span = N > 2 ? t[N - 2] - t[0] : 0.0;
+  if (N > 2 && span > 0.0 && std::isfinite(span)) {
+    for (uint32_t m = 1; m <= 8; ++m) {
+      const uint32_t cand = static_cast<uint32_t>(m * N);
+      const float a = static_cast<float>(cand / span);
+      const float b = static_cast<float>(-t[0] * (cand / span));
+      if (!std::isfinite(a) || !std::isfinite(b)) break;
+      uint32_t prev = 0xFFFFFFFFu, run = 0, worst = 0;
+      for (uint64_t c = 0; c + 1 < N; ++c) {
+        const uint32_t bb = qt::fbucket(static_cast<float>(t[c]), a, b, cand - 1);
+        run = bb == prev ? run + 1 : 1;
+        prev = bb;
+        worst = std::max(worst, run);
+      }
+      nb = cand;
+      bk_a = a;
+      bk_b = b;
+      if (worst <= 1) break;
+    }
+  }
+  h.bk_a = bk_a;
+  h.bk_b = bk_b;
+  h.nb1 = nb - 1;
+  h.bytes = round16(sizeof(qt::FastHdr) + 16ull * nb);
+  std::vector<uint8_t> out(h.bytes, 0);
+  std::memcpy(out.data(), &h, sizeof h);
+  qt::FRec* R = reinterpret_cast<qt::FRec*>(out.data() + sizeof(qt::FastHdr));
+  const float inf = std::numeric_limits<float>::infinity();
+  uint64_t c = 0;
+  for (uint32_t b = 0; b < nb; ++b) {
+    while (c + 1 < N && qt::fbucket(static_cast<float>(t[c]), bk_a, bk_b, nb - 1) < b) ++c;
+    qt::FRec r;
+    r.tl = c ? f32_up(t[c - 1]) : -inf;
+    r.t0 = f32_down(t[c]);
+    r.t1 = c + 1 < N ? f32_down(t[c + 1]) : inf;
+    r.o0 = static_cast<uint16_t>(ord[c]);
+    r.o1 = static_cast<uint16_t>(ord[std::min<uint64_t>(c + 1, N - 1)]);
+    R[b] = r;
+  }
+  return out;
+}
 
 // One layer's table (layout in qt_layout.h). header.cold_off is patched by
 // the caller once the cold block's position is known.
-TableBlob build_table(int dim, uint64_t npts, const double* pts, const double* step,
+TableBlob build_table(int kind, int dim, uint64_t npts, const double* pts, const double* step,
                       const double* marg_prev, uint64_t joff, uint64_t n_prev, uint32_t layer) {
   LayerTable h{};
+  if (kind == QT_CHAIN_BROWNIAN_1D) {  // x' = x + s eps
+    h.fa = 1.0f;
+    h.fs = f32_up_abs(step[0]);
+  } else if (kind == QT_CHAIN_OU_1D) {  // x' = a x + s eps
+    h.fa = f32_up_abs(step[0]);
+    h.fs = f32_up_abs(step[2]);
+  }
   std::memcpy(h.step, step, sizeof h.step);
   std::memcpy(h.marg_prev, marg_prev, sizeof h.marg_prev);
   h.joff = joff;
@@ -402,6 +505,8 @@ TableBlob build_table(int dim, uint64_t npts, const double* pts, const double* s
     }
     h.lo = lo;
     h.inv_w = inv_w;
+    h.bk_a = static_cast<float>(inv_w);
+    h.bk_b = static_cast<float>(-lo * inv_w);
     h.x_safe = x_safe;
     h.nb = nb;
     h.nb_d = static_cast<double>(nb);
@@ -409,14 +514,18 @@ TableBlob build_table(int dim, uint64_t npts, const double* pts, const double* s
     h.bytes = round16(h.off_start + 2ull * nb);
     out.hot.assign(h.bytes, 0);
     qt::Thr* T = reinterpret_cast<qt::Thr*>(out.hot.data() + h.off_rec);
-    for (uint64_t c = 0; c < npts; ++c) T[c] = qt::Thr{t[c], ord[c], 0};
-    T[npts] = qt::Thr{std::numeric_limits<double>::infinity(), ord[npts - 1], 0};
+    const float ninf = -std::numeric_limits<float>::infinity();
+    for (uint64_t c = 0; c < npts; ++c) T[c] = qt::Thr{t[c], ord[c], c ? f32_up(t[c - 1]) : ninf};
+    T[npts] = qt::Thr{std::numeric_limits<double>::infinity(), ord[npts - 1],
+                      f32_up(t[npts - 1])};
     uint16_t* start = reinterpret_cast<uint16_t*>(out.hot.data() + h.off_start);
     uint64_t c = 0;
     for (uint32_t b = 0; b < nb; ++b) {
       while (c + 1 < npts && qt::bucket_of(t[c], lo, inv_w, h.nb_d, nb) < b) ++c;
       start[b] = static_cast<uint16_t>(std::min<uint64_t>(c, 65535));
     }
+    if ((kind == QT_CHAIN_BROWNIAN_1D || kind == QT_CHAIN_OU_1D) && npts <= 65535)
+      out.fast = build_fast_table(kind, t, ord, x_safe, step, joff);
     out.cold.assign(16ull * npts, 0);
     Rec1* R = reinterpret_cast<Rec1*>(out.cold.data());
     for (uint64_t s = 0; s < npts; ++s) R[s] = Rec1{v[s], ord[s], 0};
@@ -458,9 +567,30 @@ struct qt_plan {
   uint32_t* d_tab_bytes = nullptr;
   uint64_t* d_fin = nullptr;  // rows, cols, joff, voff_row, voff_col (5 x n)
   std::vector<uint8_t> host_tables;
+  // fast 1-D path: replay list + counters (FastArgs::stats), paths sent to it
+  unsigned long long* d_amb = nullptr;
+  unsigned long long* d_stats = nullptr;
+  uint8_t* d_ftables = nullptr;  // fast-path tables (d == 1), concatenated
+  uint32_t* d_ftab_off = nullptr;
+  uint32_t* d_ftab_bytes = nullptr;
+  uint32_t max_ftab = 0, total_ftab = 0;
+  uint64_t amb_cap = 0, fast_paths = 0;
 
   ~qt_plan() {
     cudaSetDevice(device);
+    if (d_stats) {
+      unsigned long long st[3] = {0, 0, 0};
+      if (cudaMemcpy(st, d_stats, sizeof st, cudaMemcpyDeviceToHost) == cudaSuccess) {
+        g_fast_replayed.fetch_add(st[1]);
+        g_fast_inline.fetch_add(st[2]);
+      }
+      g_fast_paths.fetch_add(fast_paths);
+    }
+    cudaFree(d_amb);
+    cudaFree(d_stats);
+    cudaFree(d_ftables);
+    cudaFree(d_ftab_off);
+    cudaFree(d_ftab_bytes);
     cudaFree(d_tables);
     cudaFree(d_tab_off);
     cudaFree(d_tab_bytes);
@@ -509,7 +639,7 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
     if (N == 0 || N > 0xFFFFFFF0ull)
       raise(QT_ERR_NUMERIC, "grid: point data size is not a positive multiple of dim");
     check_grid(p->dim, N, pts, k);
-    blobs.push_back(build_table(p->dim, N, pts, chain->step + 6 * (k - 1),
+    blobs.push_back(build_table(p->kind, p->dim, N, pts, chain->step + 6 * (k - 1),
                                 chain->marginal + 6 * (k - 1), p->joff[k - 1], p->sizes[k - 1],
                                 static_cast<uint32_t>(k)));
     const auto& t = blobs.back().hot;
@@ -524,6 +654,20 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
     pts += N * p->dim;
   }
   p->total_tab = static_cast<uint32_t>(p->host_tables.size());
+  // fast-path tables (every layer must have one)
+  std::vector<uint8_t> ftables;
+  std::vector<uint32_t> foff, fbytes;
+  bool have_fast = true;
+  for (const TableBlob& b : blobs) have_fast = have_fast && !b.fast.empty();
+  if (have_fast) {
+    for (const TableBlob& b : blobs) {
+      foff.push_back(static_cast<uint32_t>(ftables.size()));
+      fbytes.push_back(static_cast<uint32_t>(b.fast.size()));
+      p->max_ftab = std::max<uint32_t>(p->max_ftab, static_cast<uint32_t>(b.fast.size()));
+      ftables.insert(ftables.end(), b.fast.begin(), b.fast.end());
+    }
+    p->total_ftab = static_cast<uint32_t>(ftables.size());
+  }
   // cold blocks after all hot tables; patch each header's cold_off
   for (int k = 1; k <= n; ++k) {
     TableBlob& b = blobs[k - 1];
@@ -541,6 +685,14 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
   QT_CUDA(cudaMalloc(&p->d_tables, p->host_tables.size()));
   QT_CUDA(cudaMemcpy(p->d_tables, p->host_tables.data(), p->host_tables.size(),
                      cudaMemcpyHostToDevice));
+  if (have_fast && p->max_ftab <= kMaxTableBytes) {
+    QT_CUDA(cudaMalloc(&p->d_ftables, ftables.size()));
+    QT_CUDA(cudaMemcpy(p->d_ftables, ftables.data(), ftables.size(), cudaMemcpyHostToDevice));
+    QT_CUDA(cudaMalloc(&p->d_ftab_off, n * sizeof(uint32_t)));
+    QT_CUDA(cudaMalloc(&p->d_ftab_bytes, n * sizeof(uint32_t)));
+    QT_CUDA(cudaMemcpy(p->d_ftab_off, foff.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    QT_CUDA(cudaMemcpy(p->d_ftab_bytes, fbytes.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  }
   QT_CUDA(cudaMalloc(&p->d_tab_off, n * sizeof(uint32_t)));
   QT_CUDA(cudaMalloc(&p->d_tab_bytes, n * sizeof(uint32_t)));
   QT_CUDA(cudaMemcpy(p->d_tab_off, p->tab_off.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
@@ -592,6 +744,57 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
     a.log_stages = 0;
     const bool resident = p->total_tab <= kResidentBudget;
     const size_t smem = resident ? p->total_tab : static_cast<size_t>(p->stages) * p->max_tab;
+    const bool fast = fast_enabled() && src == QT_ENGINE_MRG32K3A && p->d_ftables &&
+                      (p->kind == QT_CHAIN_BROWNIAN_1D || p->kind == QT_CHAIN_OU_1D) &&
+                      p->n < 65536 && first + count <= (1ull << 48);
+    if (fast) {
+      // replay list: room for 1/8 of the window (ambiguous paths are a few %;
+      // an overflow is still exact, replayed inline by the path kernel)
+      uint64_t want = std::max<uint64_t>(1u << 16, count / 8 + 1);
+      if (const char* cap = std::getenv("QT_FAST_REPLAY_CAP"))  // test hook: force overflow
+        want = std::max<uint64_t>(1, std::strtoull(cap, nullptr, 10));
+      if (!p->d_stats) {
+        QT_CUDA(cudaMalloc(&p->d_stats, 3 * sizeof(unsigned long long)));
+        QT_CUDA(cudaMemset(p->d_stats, 0, 3 * sizeof(unsigned long long)));
+      }
+      if (p->amb_cap < want || std::getenv("QT_FAST_REPLAY_CAP")) {
+        QT_CUDA(cudaFree(p->d_amb));
+        p->d_amb = nullptr;
+        p->amb_cap = 0;
+        QT_CUDA(cudaMalloc(&p->d_amb, want * sizeof(unsigned long long)));
+        p->amb_cap = want;
+      }
+      int P = 2;
+      if (const char* e = std::getenv("QT_FAST_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 4 ? 4 : 2;
+      // fast tables staged by the ring (all resident when they fit)
+      const bool fres = p->total_ftab <= kResidentBudget;
+      size_t fsmem = fres ? p->total_ftab : static_cast<size_t>(2) * p->max_ftab;
+      qt::PathArgs fa_args = a;
+      int bps = qt::paths_fast_blocks_per_sm(p->kind, fres, P, fsmem);
+      uint32_t st_n = 2;
+      if (!fres) {  // ring depth: as many stages as the resident CTAs leave room for
+        const uint32_t per_cta = (200u * 1024u) / static_cast<uint32_t>(bps);
+        st_n = std::max<uint32_t>(2, std::min<uint32_t>(8, per_cta / std::max(p->max_ftab, 1u)));
+        fsmem = static_cast<size_t>(st_n) * p->max_ftab;
+        bps = qt::paths_fast_blocks_per_sm(p->kind, fres, P, fsmem);
+      }
+      uint64_t blocks = static_cast<uint64_t>(p->sm_count) * bps;
+      const uint64_t slots_per_block = static_cast<uint64_t>(qt::kPathConsumers) * P;
+      const uint64_t need = (count + slots_per_block - 1) / slots_per_block;
+      if (need < blocks) blocks = need;
+      const uint64_t T = blocks * slots_per_block;
+      fa_args.q = count / T;
+      fa_args.rem = count % T;
+      qt::FastArgs fa{fa_args, p->d_amb, p->d_stats, std::min(p->amb_cap, want),
+                      p->d_ftables, p->d_ftab_off, p->d_ftab_bytes, p->max_ftab, p->total_ftab,
+                      st_n};
+      QT_CUDA(cudaMemsetAsync(p->d_stats, 0, sizeof(unsigned long long), st));
+      QT_CUDA(qt::launch_paths_fast(p->kind, fres, P, fa, static_cast<uint32_t>(blocks), fsmem,
+                                    static_cast<uint32_t>(p->sm_count) * 4u, st));
+      p->fast_paths += count;
+      g_launches.fetch_add(2);
+      return 2;
+    }
     const int bps = qt::paths_blocks_per_sm(p->kind, src, resident, smem);
     uint64_t blocks = static_cast<uint64_t>(p->sm_count) * bps;
     const uint64_t need = (count + qt::kPathConsumers - 1) / qt::kPathConsumers;
@@ -944,7 +1147,7 @@ QT_API qt_status qt_nearest(int32_t dim, uint64_t n_points, const double* points
     if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
       raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
     double zeros[6] = {0, 0, 0, 0, 0, 0};
-    TableBlob tb = build_table(dim, n_points, points, zeros, zeros, 0, 1, 1);
+    TableBlob tb = build_table(-1, dim, n_points, points, zeros, zeros, 0, 1, 1);
     std::vector<uint8_t> t = tb.hot;
     const uint32_t hot_bytes = static_cast<uint32_t>(t.size());
     set_cold_off(t, t.size());
@@ -1015,6 +1218,59 @@ QT_API qt_status qt_uniforms(int32_t engine, uint64_t seed, uint64_t offset, uin
     if (e == cudaSuccess) e = cudaMemcpy(out, d, count * sizeof(double), cudaMemcpyDeviceToHost);
     cudaFree(d);
     QT_CUDA(e);
+  });
+}
+
+QT_API qt_status qt_set_fast_path(int32_t enabled) {
+  g_fast.store(enabled ? 1 : 0);
+  return QT_OK;
+}
+
+QT_API qt_status qt_fast_stats(uint64_t* out) {
+  return guarded([&] {
+    if (!out) raise(QT_ERR_INVALID_ARGUMENT, "null argument");
+    out[0] = g_fast_paths.load();
+    out[1] = g_fast_replayed.load();
+    out[2] = g_fast_inline.load();
+  });
+}
+
+QT_API qt_status qt_plan_fast_stats(const qt_plan* plan, uint64_t* out) {
+  return guarded([&] {
+    if (!plan || !out) raise(QT_ERR_INVALID_ARGUMENT, "null argument");
+    unsigned long long st[3] = {0, 0, 0};
+    if (plan->d_stats) {
+      QT_CUDA(cudaSetDevice(plan->device));
+      QT_CUDA(cudaDeviceSynchronize());
+      QT_CUDA(cudaMemcpy(st, plan->d_stats, sizeof st, cudaMemcpyDeviceToHost));
+    }
+    out[0] = plan->fast_paths;
+    out[1] = st[1];
+    out[2] = st[2];
+  });
+}
+
+QT_API qt_status qt_fast_bounds_check(double* out) {
+  return guarded([&] {
+    if (!out) raise(QT_ERR_INVALID_ARGUMENT, "null argument");
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+      raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
+    QT_CUDA(cudaSetDevice(0));
+    unsigned int* d = nullptr;
+    QT_CUDA(cudaMalloc(&d, 4 * sizeof(unsigned int)));
+    cudaError_t e = cudaMemset(d, 0, 4 * sizeof(unsigned int));
+    if (e == cudaSuccess) e = qt::launch_fast_bounds_check(d, nullptr);
+    unsigned int h[4] = {0, 0, 0, 0};
+    if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    QT_CUDA(e);
+    g_launches.fetch_add(1);
+    for (int i = 0; i < 4; ++i) {
+      float f;
+      std::memcpy(&f, &h[i], 4);
+      out[i] = f;
+    }
   });
 }
 

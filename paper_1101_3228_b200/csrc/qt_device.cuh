@@ -69,6 +69,36 @@ __device__ __forceinline__ uint32_t mrg_step(Mrg& s) {
   return p1 >= p2 ? p1 - p2 : p1 - p2 + kM1;  // mod-2^32 wrap gives the exact value
 }
 
+// Two consecutive outputs (x1 then x2) with the residues reduced by
+// min_u32(r, r - m): r - m wraps above r exactly when r < m.
+__device__ __forceinline__ uint32_t fold_m1(uint64_t t) {  // t < 2^54
+  const uint64_t r = mulw(static_cast<uint32_t>(t >> 32), kC1) + static_cast<uint32_t>(t);
+  const uint32_t r2 = static_cast<uint32_t>(r) + static_cast<uint32_t>(r >> 32) * kC1;
+  return min(r2, r2 - kM1);
+}
+__device__ __forceinline__ uint32_t fold_m2(uint64_t t) {  // t < 2^54
+  const uint64_t r = mulw(static_cast<uint32_t>(t >> 32), kC2) + static_cast<uint32_t>(t);
+  const uint64_t r2 = mulw(static_cast<uint32_t>(r >> 32), kC2) + static_cast<uint32_t>(r);
+  const uint32_t r3 = static_cast<uint32_t>(r2) + static_cast<uint32_t>(r2 >> 32) * kC2;
+  return min(r3, r3 - kM2);
+}
+__device__ __forceinline__ void mrg_step2(Mrg& s, uint32_t& x1, uint32_t& x2) {
+  // component 1: x_n = a12 x_{n-2} - a13n x_{n-3}; the two new values are independent
+  const uint32_t p1 = fold_m1(mulw(kA12, s.a1) + mulw(kA13n, kM1 - s.a0));
+  const uint32_t q1 = fold_m1(mulw(kA12, s.a2) + mulw(kA13n, kM1 - s.a1));
+  // component 2: x_n = a21 x_{n-1} - a23n x_{n-3}
+  const uint32_t p2 = fold_m2(mulw(kA21, s.b2) + mulw(kA23n, kM2 - s.b0));
+  const uint32_t q2 = fold_m2(mulw(kA21, p2) + mulw(kA23n, kM2 - s.b1));
+  s.a0 = s.a2;
+  s.a1 = p1;
+  s.a2 = q1;
+  s.b0 = s.b2;
+  s.b1 = p2;
+  s.b2 = q2;
+  x1 = p1 >= p2 ? p1 - p2 : p1 - p2 + kM1;
+  x2 = q1 >= q2 ? q1 - q2 : q1 - q2 + kM1;
+}
+
 // (x + 1) / (m1 + 1), correctly rounded. Division by the constant is done as
 // q = RN(a R); r = a - q d (exact, FMA); RN(q + r R): tests/test_division.py
 // proves it equals the IEEE quotient for all 2^32 possible numerators.
@@ -198,6 +228,85 @@ __device__ __forceinline__ void box_muller(double u1, double u2, double& z1, dou
   qt_sincos_2pi(a, &s, &c);
   z1 = __dmul_rn(r, c);
   z2 = __dmul_rn(r, s);
+}
+
+// ---------------------------------------------------------------------------
+// FP32 Box-Muller of the fast 1-D path (MRG32k3a only). It never decides a
+// cell by itself: it yields z~ together with a rigorous bound
+// |z~ - z| <= bz(r~) against the exact FP64 normal z of box_muller() above, and
+// the path kernel only counts a transition whose FP64 state interval
+// [x~ - e, x~ + e] lies strictly inside one cell. The bound constants below
+// are verified over ALL 2^32 MRG32k3a outputs by k_fast_bounds_check
+// (qt_fast_bounds_check, tests/test_gpu_parity.py), with the composition
+// |r~c~ - rc| <= |r~-r| |c~| + r |c~-c| + 2^-24 |z~| done analytically.
+// Every FP32 operation is an explicitly rounded intrinsic or an .approx
+// instruction (deterministic MUFU), so the kernel and the checker compute the
+// same bits.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float mufu_lg2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float mufu_sin(float x) {
+  float y;
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float mufu_cos(float x) {
+  float y;
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float mufu_sqrt(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float mufu_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// radius bound |r~ - r| <= kRadA + kRadB r~ ; angle bound |c~ - c|, |s~ - s| <= kAng
+constexpr float kRadA = 2.2e-7f;
+constexpr float kRadB = 1.6e-7f;
+constexpr float kAng = 5.5e-7f;
+// bz = kBzA + kBzB r~ >= kRadA (1 + kAng) + r~ ((kRadB (1 + kAng) + kAng + 2^-23)
+// (rounded up generously; |c~| <= 1 is also checked exhaustively)
+constexpr float kBzA = 2.21e-7f;
+constexpr float kBzB = 7.75e-7f;
+
+// r~ = sqrt(-2 ln u), u = (x + 1) / (m1 + 1), from the MRG32k3a integer x
+__device__ __forceinline__ float fast_radius(uint32_t x) {
+  const uint32_t v = kM1 - x;  // (m1 + 1) (1 - u), in (0, m1]
+  const float uf = __fmul_rn(__uint2float_rn(x + 1u), 0x1p-32f);
+  const float wf = __fmul_rn(__uint2float_rn(v), 0x1p-32f);
+  const bool lower = x < 2147483544u;  // u < 1/2: log of u itself
+  const float t = __fsub_rn(1.0f, wf);
+  const float L = mufu_lg2(lower ? uf : t);
+  // u < 1/2: -2 ln2 (log2(x+1) - 32 + log2(2^32 / (m1 + 1)))
+  const float RA = __fmaf_rn(L, -1.3862943611198906f, -9.6853e-8f);
+  // 1/8 < w <= 1/2: log1p(-w) = ln(t) w / (1 - t) corrects the rounding of t
+  const float RB = __fmul_rn(__fmul_rn(L, -1.3862943611198906f), __fmul_rn(wf, mufu_rcp(__fsub_rn(1.0f, t))));
+  // w <= 1/8: -2 ln(1 - w) = 2 w (1 + w/2 + ... + w^6/7)
+  float P = __fmaf_rn(wf, 0.14285714285714285f, 0.16666666666666666f);
+  P = __fmaf_rn(wf, P, 0.2f);
+  P = __fmaf_rn(wf, P, 0.25f);
+  P = __fmaf_rn(wf, P, 0.3333333333333333f);
+  P = __fmaf_rn(wf, P, 0.5f);
+  P = __fmaf_rn(wf, P, 1.0f);
+  const float RS = __fmul_rn(__fmul_rn(2.0f, wf), P);
+  return mufu_sqrt(lower ? RA : (wf <= 0.125f ? RS : RB));
+}
+
+// (c~, s~) = (cos, sin)(2 pi u) as -(cos, sin)(2 pi (u - 1/2))
+__device__ __forceinline__ void fast_angle(uint32_t x, float& c, float& s) {
+  const int d = static_cast<int>(x + 1u - 2147483544u);  // (m1 + 1)(u - 1/2), exact
+  const float a = __fmul_rn(__int2float_rn(d), 1.4629180792671596e-09f);  // 2 pi / (m1 + 1)
+  c = -mufu_cos(a);
+  s = -mufu_sin(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -505,6 +614,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "r"(a), "r"(parity), "r"(0x100000u)  // suspend (not spin) up to ~1 ms
         : "memory");
   } while (!done);
+}
+
+// The same on a precomputed shared-window address (no per-call cvta).
+__device__ __forceinline__ void mbar_wait_u32(uint32_t a, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity), "r"(0x100000u)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
 
 // bytes must be a multiple of 16, both addresses 16-byte aligned.

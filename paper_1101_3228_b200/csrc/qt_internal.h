@@ -40,6 +40,21 @@ struct PathArgs {
 
 constexpr int kPathConsumers = 256;  // consumer threads per k_paths CTA
 
+// Fast 1-D path (FP32 Box-Muller with certified cells + exact replay).
+struct FastArgs {
+  PathArgs p;
+  unsigned long long* amb;    // ambiguous paths: (path << 16) | first uncertified layer
+  unsigned long long* stats;  // [0] entries of this launch, [1] replayed (cumulative),
+                              // [2] replayed inline on list overflow (cumulative)
+  uint64_t cap;               // capacity of amb
+  const uint8_t* ftables;     // fast-path tables (FastHdr + FRec[]), concatenated
+  const uint32_t* ftab_off;   // [n]
+  const uint32_t* ftab_bytes; // [n]
+  uint32_t fbuf_bytes;        // ring stage size (max fast table)
+  uint32_t fresident_bytes;   // sum of fast tables (resident mode)
+  uint32_t fstages;           // ring depth
+};
+
 struct Alg3Args {
   SrcArgs src;
   const uint8_t* tables;
@@ -67,6 +82,10 @@ void note_launches(uint64_t n);
 cudaError_t launch_paths(int kind, int src, bool resident, const PathArgs& a, uint32_t blocks,
                          size_t smem, cudaStream_t st);
 int paths_blocks_per_sm(int kind, int src, bool resident, size_t smem);
+cudaError_t launch_paths_fast(int kind, bool resident, int P, const FastArgs& a, uint32_t blocks,
+                              size_t smem, uint32_t replay_blocks, cudaStream_t st);
+int paths_fast_blocks_per_sm(int kind, bool resident, int P, size_t smem);
+cudaError_t launch_fast_bounds_check(unsigned int* out, cudaStream_t st);
 cudaError_t launch_alg3(int kind, int src, const Alg3Args& a, uint32_t slices, size_t smem,
                         cudaStream_t st);
 cudaError_t launch_finalize(bool alg3, const unsigned long long* joint, unsigned long long* visits,

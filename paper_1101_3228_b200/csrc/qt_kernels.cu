@@ -134,6 +134,289 @@ __global__ void __launch_bounds__(kPathThreads) k_paths(const PathArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Fast 1-D path (Brownian / OU chains, MRG32k3a): the same warp-specialised
+// ring as k_paths, but the normals come from the FP32 Box-Muller of
+// qt_device.cuh with a rigorous error bound, the state x~ is carried in FP64
+// together with an FP32 bound e >= |x~ - x| on the exact kernel's state x, and
+// a transition is counted only when [x~ - e, x~ + e] lies inside one cell
+// (t_{c-1} <= x~ - e, x~ + e < t_c). The first uncertified transition of a
+// path ends its counting here; the path is appended to the replay list and
+// k_replay recomputes it with the exact FP64 arithmetic of k_paths, counting
+// from that layer on. The counts are therefore identical to k_paths' counts.
+// ---------------------------------------------------------------------------
+
+// Exact FP64 recomputation of path `path` (the body of k_paths, tables read
+// from global memory), counting transitions k >= k0.
+template <int K>
+__device__ __noinline__ void replay_path(const PathArgs& a, uint64_t path, uint32_t k0) {
+  using C = Chain<K>;
+  Source<kSrcMrg> src;
+  src.start(a.src, path);
+  double x[1] = {0.0};
+  uint32_t i = 0;
+  for (uint32_t k = 1; k <= a.n; ++k) {
+    const uint8_t* tb = a.tables + __ldg(a.tab_off + k - 1);
+    const LayerTable& h = *reinterpret_cast<const LayerTable*>(tb);
+    double e[1], xn[1];
+    e[0] = src.normal();
+    C::step(h.step, x, xn, e);
+    x[0] = xn[0];
+    const uint32_t j = nearest_1d(h, tb, x[0], a.tables);
+    if (k >= k0) red_add_u64(a.joint + h.joff + static_cast<uint64_t>(i) * h.n_pts + j, 1ull);
+    i = j;
+  }
+}
+
+// Per-slot state of the fast kernel (one path in flight).
+struct FastPath {
+  Mrg st;
+  uint64_t beg, count;  // this slot's contiguous run of paths
+  double x;             // x~
+  float e;              // |x~ - x| <= e
+  float xs;             // x~ rounded to FP32 (bucket + rounding term)
+  float zs, bzs;        // Box-Muller mate and its bound
+  uint32_t i;           // cell at the previous layer
+  uint32_t amb_k;       // first uncertified layer (0: none so far)
+};
+
+// One layer k for the P slots of a thread, against the layer's fast table
+// (FastHdr + FRec[], qt_layout.h). Written as straight-line phases over the
+// slots, so the compiler interleaves the P independent dependency chains.
+// Per transition: one 16-byte shared-memory record and FP32 compares decide
+// and certify the cell; nothing on this path is FP64 except the state x~.
+template <int K, int P>
+__device__ __forceinline__ void fast_layer(FastPath (&ps)[P], const bool (&act)[P],
+                                           const uint8_t* tb, uint32_t k,
+                                           unsigned long long* joint) {
+  const FastHdr& h = *reinterpret_cast<const FastHdr*>(tb);
+  const double c0 = h.c0;
+  const double c2 = K == 0 ? 0.0 : h.c2;
+  const float fa = h.fa, fs = h.fs, bk_a = h.bk_a, bk_b = h.bk_b, x_safe = h.x_safe;
+  const uint32_t nb1 = h.nb1, npts = h.n_pts;
+  const FRec* R = reinterpret_cast<const FRec*>(tb + sizeof(FastHdr));
+  unsigned long long* jl = joint + h.joff;
+
+  float z[P], bz[P];
+  if (k & 1u) {  // a fresh pair (stream.hpp:97-108): z = r cos, mate = r sin
+    uint32_t u1[P], u2[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) mrg_step2(ps[p].st, u1[p], u2[p]);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const float rr = fast_radius(u1[p]);
+      float c, sn;
+      fast_angle(u2[p], c, sn);
+      z[p] = __fmul_rn(rr, c);
+      ps[p].zs = __fmul_rn(rr, sn);
+      bz[p] = __fmaf_ru(kBzB, rr, kBzA);
+      ps[p].bzs = bz[p];
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      z[p] = ps[p].zs;
+      bz[p] = ps[p].bzs;
+    }
+  }
+  FRec rec[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const double zd = static_cast<double>(z[p]);
+    double xn;
+    if constexpr (K == 0) xn = __fma_rn(c0, zd, ps[p].x);            // x + s eps
+    else xn = __fma_rn(c0, ps[p].x, __dmul_rn(c2, zd));             // a x + s eps
+    const float xns = __double2float_rn(xn);
+    // e' = fa e + fs bz + 2^-49 (|x| + 2 |x'|): the FP64 roundings of both
+    // recurrences (|x| <= |xs| (1 + 2^-23)); fs |z| 2^-50 is inside kBzB's slack
+    ps[p].e = __fmaf_ru(fa, ps[p].e,
+                        __fmaf_ru(fs, bz[p], __fmul_ru(0x1p-49f, __fmaf_ru(2.0f, fabsf(xns),
+                                                                            fabsf(ps[p].xs)))));
+    ps[p].x = xn;
+    ps[p].xs = xns;
+    rec[p] = R[fbucket(xns, bk_a, bk_b, nb1)];
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const float xs = ps[p].xs;
+    // [x~ - e, x~ + e] inside [xl, xh]: E also covers |xs - x~| <= 2^-24 |x~|
+    const float E = __fmaf_ru(fabsf(xs), 0x1p-23f, ps[p].e);
+    const float xl = __fadd_rd(xs, -E), xh = __fadd_ru(xs, E);
+    const FRec& r = rec[p];
+    const bool lo = xs < r.t0;
+    const float up0 = __int_as_float(__float_as_int(r.t0) + (r.t0 >= 0.0f ? 1 : -1));  // >= t_c
+    const float lb = lo ? r.tl : up0;
+    const float ub = lo ? r.t0 : r.t1;
+    const uint32_t cell = lo ? r.o0 : r.o1;
+    const bool ok = xl >= lb && xh < ub && __fadd_ru(fabsf(xs), E) < x_safe;
+    const bool live = act[p] && ps[p].amb_k == 0;
+    if (live && ok) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + cell, 1ull);
+    ps[p].i = cell;
+    if (live && !ok) ps[p].amb_k = k;
+  }
+}
+
+template <int K, bool RESIDENT, int P>
+__global__ void __launch_bounds__(kPathThreads) k_paths_fast(const __grid_constant__ FastArgs f) {
+  const PathArgs& a = f.p;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[kMaxStages];
+  __shared__ __align__(8) uint64_t empty[kMaxStages];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+  const uint32_t S = f.fstages;
+  const uint64_t rounds = a.q + (a.rem ? 1u : 0u);
+  const uint64_t steps_total = rounds * a.n;
+  if (steps_total == 0) return;
+
+  if (tid == 0) {
+    for (uint32_t s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {  // ---- producer warp (as k_paths) ----
+    if (lane == 0) {
+      if constexpr (RESIDENT) {
+        mbar_expect_tx(&full[0], f.fresident_bytes);
+        for (uint32_t k = 0; k < a.n; ++k)
+          bulk_g2s(smem + f.ftab_off[k], f.ftables + f.ftab_off[k], f.ftab_bytes[k], &full[0]);
+      } else {
+        uint32_t k = 0, s = 0, ph = 0;
+        for (uint64_t g = 0; g < steps_total; ++g) {
+          mbar_wait(&empty[s], ph ^ 1u);
+          const uint32_t bytes = __ldg(f.ftab_bytes + k);
+          mbar_expect_tx(&full[s], bytes);
+          bulk_g2s(smem + s * f.fbuf_bytes, f.ftables + __ldg(f.ftab_off + k), bytes, &full[s]);
+          k = k + 1 == a.n ? 0 : k + 1;
+          if (++s == S) {
+            s = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // P slots per consumer thread: slot v = gid P + p owns a contiguous run of
+  // paths (the window split over T P slots), so each slot's stream flows from
+  // path to path without jumps; the P slots share the layer wait.
+  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * kConsumers + tid;
+  FastPath ps[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const uint64_t v = gid * P + p;
+    ps[p].count = a.q + (v < a.rem ? 1u : 0u);
+    ps[p].beg = a.first + v * a.q + (v < a.rem ? v : a.rem);
+    ps[p].st = Mrg{};
+    if (ps[p].count) {
+      Source<kSrcMrg> src;
+      src.start(a.src, ps[p].beg);
+      ps[p].st = src.s;
+    }
+  }
+  if constexpr (RESIDENT) mbar_wait(&full[0], 0);
+  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
+  uint32_t s = 0, ph = 0;
+  const uint8_t* tb = smem;
+  for (uint64_t r = 0; r < rounds; ++r) {
+    bool act[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      act[p] = r < ps[p].count;
+      ps[p].x = 0.0;  // chains.hpp:43-46,81: the origin
+      ps[p].e = 0.0f;
+      ps[p].xs = 0.0f;
+      ps[p].i = 0;
+      ps[p].amb_k = 0;
+    }
+    for (uint32_t k = 1; k <= a.n; ++k) {
+      if constexpr (RESIDENT) {
+        tb = smem + f.ftab_off[k - 1];
+      } else {
+        mbar_wait_u32(full0 + 8u * s, ph);
+      }
+      fast_layer<K, P>(ps, act, tb, k, a.joint);
+      if constexpr (!RESIDENT) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(empty0 + 8u * s);
+        tb += f.fbuf_bytes;
+        if (++s == S) {
+          s = 0;
+          ph ^= 1u;
+          tb = smem;
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (act[p] && ps[p].amb_k != 0) {
+        const uint64_t path = ps[p].beg + r;
+        const unsigned long long idx = atomicAdd(f.stats, 1ull);
+        if (idx < f.cap) {
+          f.amb[idx] = (path << 16) | ps[p].amb_k;
+        } else {  // list full: replay here (correct, slow; never expected)
+          replay_path<K>(a, path, ps[p].amb_k);
+          atomicAdd(f.stats + 2, 1ull);
+        }
+      }
+    }
+  }
+}
+
+// The replay list of one k_paths_fast launch, grid-stride.
+template <int K>
+__global__ void __launch_bounds__(256) k_replay(const __grid_constant__ FastArgs f) {
+  const unsigned long long entries = *reinterpret_cast<volatile unsigned long long*>(f.stats);
+  const uint64_t n = entries < f.cap ? entries : f.cap;
+  const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g0 == 0) atomicAdd(f.stats + 1, static_cast<unsigned long long>(n));
+  for (uint64_t g = g0; g < n; g += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long ent = f.amb[g];
+    replay_path<K>(f.p, ent >> 16, static_cast<uint32_t>(ent & 0xFFFFu));
+  }
+}
+
+// Exhaustive check of the FP32 Box-Muller bounds over all 2^32 - 209 MRG32k3a
+// outputs x (both u1 and u2 roles): out[0] = max(|r~ - r| - kRadB r~),
+// out[1] = max |c~ - c|, out[2] = max |s~ - s|, out[3] = max(|c~|, |s~|),
+// as FP32 bit patterns (non-negative floats order like their bits).
+__global__ void __launch_bounds__(256) k_fast_bounds_check(unsigned int* out) {
+  float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+  for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < kM1;
+       g += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t x = static_cast<uint32_t>(g);
+    const double u = mrg_to_unit(x);
+    const double r = __dsqrt_rn(__dmul_rn(-2.0, qt_log_unit(u)));
+    const float rt = fast_radius(x);
+    const double dr = fabs(static_cast<double>(rt) - r) - static_cast<double>(kRadB) * rt;
+    m0 = fmaxf(m0, __double2float_ru(dr));
+    double sn, cs;
+    qt_sincos_2pi(__dmul_rn(kTwoPi, u), &sn, &cs);
+    float c, s;
+    fast_angle(x, c, s);
+    m1 = fmaxf(m1, __double2float_ru(fabs(static_cast<double>(c) - cs)));
+    m2 = fmaxf(m2, __double2float_ru(fabs(static_cast<double>(s) - sn)));
+    m3 = fmaxf(m3, fmaxf(fabsf(c), fabsf(s)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+    m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    m2 = fmaxf(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+    m3 = fmaxf(m3, __shfl_xor_sync(0xffffffffu, m3, o));
+  }
+  if ((threadIdx.x & 31u) == 0) {
+    atomicMax(out + 0, __float_as_uint(m0));
+    atomicMax(out + 1, __float_as_uint(m1));
+    atomicMax(out + 2, __float_as_uint(m2));
+    atomicMax(out + 3, __float_as_uint(m3));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Alg III: grid = (slices, n). Slice s of layer k covers samples
 // [M s / S, M (s+1) / S) of that layer; each thread a contiguous sub-run, so
 // its stream again flows sample to sample without jumps.
@@ -361,6 +644,62 @@ int paths_blocks_per_sm(int kind, int src, bool resident, size_t smem) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kPathThreads, smem) != cudaSuccess)
     return 1;
   return nb > 0 ? nb : 1;
+}
+
+template <int K, bool RES, int P>
+static cudaError_t launch_fast_t(const FastArgs& a, dim3 grid, size_t smem, uint32_t rblocks,
+                                 cudaStream_t st) {
+  auto fn = k_paths_fast<K, RES, P>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  fn<<<grid, kPathThreads, smem, st>>>(a);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_replay<K><<<rblocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int K, int P>
+static const void* fast_fn(bool res) {
+  return res ? reinterpret_cast<const void*>(k_paths_fast<K, true, P>)
+             : reinterpret_cast<const void*>(k_paths_fast<K, false, P>);
+}
+
+template <int K>
+static cudaError_t launch_fast_k(bool res, int P, const FastArgs& a, dim3 g, size_t smem,
+                                 uint32_t rb, cudaStream_t st) {
+  switch (P) {
+    case 1: return res ? launch_fast_t<K, true, 1>(a, g, smem, rb, st)
+                       : launch_fast_t<K, false, 1>(a, g, smem, rb, st);
+    case 4: return res ? launch_fast_t<K, true, 4>(a, g, smem, rb, st)
+                       : launch_fast_t<K, false, 4>(a, g, smem, rb, st);
+    default: return res ? launch_fast_t<K, true, 2>(a, g, smem, rb, st)
+                        : launch_fast_t<K, false, 2>(a, g, smem, rb, st);
+  }
+}
+
+// k_paths_fast + k_replay (kind 0 = Brownian, 2 = OU); P paths in flight per thread
+cudaError_t launch_paths_fast(int kind, bool resident, int P, const FastArgs& a, uint32_t blocks,
+                              size_t smem, uint32_t replay_blocks, cudaStream_t st) {
+  const dim3 g(blocks);
+  return kind == 0 ? launch_fast_k<0>(resident, P, a, g, smem, replay_blocks, st)
+                   : launch_fast_k<2>(resident, P, a, g, smem, replay_blocks, st);
+}
+
+int paths_fast_blocks_per_sm(int kind, bool resident, int P, size_t smem) {
+  const void* fn;
+  if (kind == 0) fn = P == 1 ? fast_fn<0, 1>(resident) : P == 4 ? fast_fn<0, 4>(resident) : fast_fn<0, 2>(resident);
+  else fn = P == 1 ? fast_fn<2, 1>(resident) : P == 4 ? fast_fn<2, 4>(resident) : fast_fn<2, 2>(resident);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kPathThreads, smem) != cudaSuccess)
+    return 1;
+  return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_fast_bounds_check(unsigned int* out, cudaStream_t st) {
+  k_fast_bounds_check<<<148 * 16, 256, 0, st>>>(out);
+  return cudaGetLastError();
 }
 
 template <int K, int SRC>

@@ -5,7 +5,8 @@
 // part, staged into shared memory):
 //
 //   LayerTable header (192 B)
-//   d == 1 : Thr[N + 1]        per sorted cell c: {t_c, original index of c};
+//   d == 1 : Thr[N + 1]        per sorted cell c: {t_c, original index of c,
+//                              t_{c-1} rounded up to FP32};
 //                              t_c is the exact FP64 decision threshold between
 //                              sorted cells c and c+1 (t_{N-1} = t_N = +inf)
 //            uint16 start[nb]  bucket b -> #{thresholds whose bucket < b}
@@ -20,6 +21,9 @@
 // CTA that holds a layer's table in shared memory has everything one step needs.
 #pragma once
 #include <stdint.h>
+#if !defined(__CUDA_ARCH__)
+#include <cmath>
+#endif
 
 namespace qt {
 
@@ -40,14 +44,18 @@ struct alignas(16) LayerTable {
   uint32_t bytes;       // hot table bytes (multiple of 16)
   uint32_t layer;       // k
   uint32_t dim;
-  uint32_t pad_[4];
+  float fa;             // d == 1 fast path: |a| of x' = a x + s eps, rounded up (FP32)
+  float fs;             // d == 1 fast path: |s|, rounded up (FP32)
+  float bk_a, bk_b;     // d == 1 fast path: approximate bucket fma(x, bk_a, bk_b)
+                        // (FP32; any start cell is fine there, certification decides)
 };
 static_assert(sizeof(LayerTable) == 192, "LayerTable header is 192 bytes");
 
 struct alignas(16) Thr {
   double t;
   uint32_t orig;
-  uint32_t pad;
+  float tp;  // t_{c-1} rounded UP to FP32 (-inf for c = 0): x >= tp implies
+             // x >= t_{c-1}, the fast path's lower certification bound for cell c
 };
 static_assert(sizeof(Thr) == 16, "Thr is 16 bytes");
 
@@ -57,6 +65,52 @@ struct alignas(16) Rec1 {
   uint32_t pad;
 };
 static_assert(sizeof(Rec1) == 16, "Rec1 is 16 bytes");
+
+// ---------------------------------------------------------------------------
+// Fast-path layer table (d == 1 only; k_paths_fast). One 16-byte record per
+// bucket of an FP32 bucket map b(x) = min(u32_rz(fmaf(fl32(x), bk_a, bk_b)),
+// nb - 1), the SAME IEEE operations on host and device. With c = #{thresholds
+// t whose b(t) < b} (monotonicity of b gives t_{c-1} < x for every x in bucket
+// b), the record holds the thresholds around c rounded OUTWARD to FP32 and the
+// original indices of cells c and c + 1, so one 16-byte shared-memory load
+// decides and certifies a transition:
+//   x in [xl, xh], xh < t0      and xl >= tl      -> cell o0
+//   x in [xl, xh], xh < t1      and xl >= up(t0)  -> cell o1
+// (any other case is left uncertified -> exact replay).
+// ---------------------------------------------------------------------------
+struct alignas(16) FastHdr {
+  double c0, c2;      // step coefficients: Brownian x + c0 eps; OU c0 x + c2 eps
+  uint64_t joff;      // element offset of joint[k-1]
+  float fa, fs;       // |a|, |s| rounded up
+  float bk_a, bk_b;   // FP32 bucket map
+  float x_safe;       // exact-kernel x_safe rounded down (0: never certify)
+  uint32_t nb1;       // buckets - 1
+  uint32_t n_pts;     // N_k
+  uint32_t bytes;     // table bytes (multiple of 16)
+};
+static_assert(sizeof(FastHdr) == 64, "FastHdr is 64 bytes");
+
+struct alignas(16) FRec {
+  float tl;            // t_{c-1} rounded up (-inf for c = 0)
+  float t0;            // t_c rounded down (never -0)
+  float t1;            // t_{c+1} rounded down (+inf past the last cell)
+  uint16_t o0, o1;     // original indices of cells c, c + 1
+};
+static_assert(sizeof(FRec) == 16, "FRec is 16 bytes");
+
+// The FP32 bucket map shared by host (table build) and device (query).
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline uint32_t fbucket(float xs, float bk_a, float bk_b, uint32_t nb1) {
+#if defined(__CUDA_ARCH__)
+  const uint32_t b = __float2uint_rz(__fmaf_rn(xs, bk_a, bk_b));
+#else
+  const float v = std::fmaf(xs, bk_a, bk_b);
+  const uint32_t b = !(v > 0.0f) ? 0u : (v >= 4294967296.0f ? 0xFFFFFFFFu : static_cast<uint32_t>(v));
+#endif
+  return b < nb1 ? b : nb1;
+}
 
 constexpr uint32_t kNoIndex = 0xFFFFFFFFu;
 

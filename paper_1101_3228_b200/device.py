@@ -69,5 +69,12 @@ class Plan:
         return n.value
 
 
+    def fast_stats(self) -> dict:
+        """Fast 1-D path evidence of this plan (synchronises its device)."""
+        out = (C.c_uint64 * 3)()
+        _check(L.lib().qt_plan_fast_stats(self._h, out), "plan_fast_stats")
+        return {"fast_paths": int(out[0]), "replayed": int(out[1]), "inline_replayed": int(out[2])}
+
+
 def units_total(estimator, chain, samples: int) -> int:
     return samples * chain.layers() if int(estimator) == EstimatorKind.AlgIII else samples

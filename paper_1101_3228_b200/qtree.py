@@ -389,6 +389,25 @@ def path_normals(engine, seed, normals_per_path, first, count) -> np.ndarray:
     return out
 
 
+def set_fast_path(enabled: bool) -> None:
+    """Select the fast 1-D path (FP32 Box-Muller + certified cells + exact
+    replay; identical counts) or the exact FP64 kernel for every path."""
+    L.lib().qt_set_fast_path(1 if enabled else 0)
+
+
+def fast_stats() -> dict:
+    out = (C.c_uint64 * 3)()
+    _check(L.lib().qt_fast_stats(out), "fast_stats")
+    return {"fast_paths": int(out[0]), "replayed": int(out[1]), "inline_replayed": int(out[2])}
+
+
+def fast_bounds_check() -> np.ndarray:
+    """Exhaustive device check of the FP32 Box-Muller error bounds."""
+    out = np.zeros(4, np.float64)
+    _check(L.lib().qt_fast_bounds_check(_f(out)), "fast_bounds_check")
+    return out
+
+
 def uniforms(engine, seed, offset, count) -> np.ndarray:
     out = np.zeros(int(count), np.float64)
     _check(L.lib().qt_uniforms(int(engine), int(seed), int(offset), int(count), _f(out)),

@@ -1,0 +1,132 @@
+"""The fast 1-D path (FP32 Box-Muller + certified cells + exact FP64 replay).
+
+Its contract is that the counts are IDENTICAL to the exact kernel's (k_paths)
+for every input: a transition is counted only when the bounded state interval
+lies inside one cell, and every path with an uncertified transition is
+recomputed exactly from that layer on. These tests check (1) the FP32 error
+bounds exhaustively over all 2^32 MRG32k3a outputs, (2) fast == exact on the
+configs and on adversarial grids, including the replay-list overflow path, and
+(3) fast == the CPU oracle on fresh windows (the other parity tests in
+test_gpu_parity.py also run through the fast path, which is the default)."""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from pyoracle import CHAIN_BROWNIAN1D, CHAIN_OU1D, ChainSpec
+
+pytestmark = pytest.mark.gpu
+
+# qt_device.cuh: kRadA, kRadB, kAng
+K_RAD_A, K_ANG = 2.2e-7, 5.5e-7
+
+
+def Q():
+    from paper_1101_3228_b200 import qtree
+    return qtree
+
+
+def _counts(plan, M, first=0, total=None, fast=True):
+    import torch
+    q = Q()
+    q.set_fast_path(fast)
+    try:
+        joint = plan.zeros_joint()
+        plan.count(1, 1, 12345, first, M, total or M, joint)
+        torch.cuda.synchronize()
+        return joint.cpu().numpy().view(np.uint64).copy()
+    finally:
+        q.set_fast_path(True)
+
+
+def test_fp32_box_muller_bounds_exhaustive(gpu):
+    out = Q().fast_bounds_check()
+    assert out[0] <= K_RAD_A, out
+    assert out[1] <= K_ANG and out[2] <= K_ANG, out
+    assert out[3] <= 1.0, out
+
+
+def test_fast_equals_exact_c2(gpu):
+    from paper_1101_3228_b200.device import Plan
+    q = Q()
+    ch = q.BrownianChain1d(50)
+    plan = Plan(ch, q.build_brownian_grids(ch, 500), 0)
+    for first in (0, 987654321):
+        fast = _counts(plan, 2 * 10**6, first, 10**9, True)
+        exact = _counts(plan, 2 * 10**6, first, 10**9, False)
+        assert np.array_equal(fast, exact), first
+    st = plan.fast_stats()
+    assert st["fast_paths"] == 4 * 10**6
+    # the replay path is exercised (a few % of paths are not certified)
+    assert 0 < st["replayed"] < 4 * 10**5, st
+    assert st["inline_replayed"] == 0, st
+
+
+def test_fast_equals_exact_ou(gpu):
+    from paper_1101_3228_b200.device import Plan
+    q = Q()
+    p = q.TwoFactorParams(sigma1=0.5, alpha1=1.0, sigma2=0.0, steps=365)
+    ch = q.OuChain1d(p)
+    plan = Plan(ch, q.build_ou_grids(ch, 200), 0)
+    assert np.array_equal(_counts(plan, 200000, 0, 10**6, True),
+                          _counts(plan, 200000, 0, 10**6, False))
+
+
+def test_fast_replay_list_overflow(gpu, monkeypatch):
+    """A replay list of 3 entries: every further ambiguous path is replayed
+    inline by the path kernel; the counts do not change."""
+    from paper_1101_3228_b200.device import Plan
+    q = Q()
+    ch = q.BrownianChain1d(50)
+    grids = q.build_brownian_grids(ch, 500)
+    exact = _counts(Plan(ch, grids, 0), 300000, 5, 10**9, False)
+    monkeypatch.setenv("QT_FAST_REPLAY_CAP", "3")
+    plan = Plan(ch, grids, 0)
+    fast = _counts(plan, 300000, 5, 10**9, True)
+    st = plan.fast_stats()
+    assert np.array_equal(fast, exact)
+    assert st["replayed"] == 3 and st["inline_replayed"] > 0, st
+
+
+@pytest.mark.parametrize("case", ["dense", "single", "tiny_gap", "huge_spread"])
+def test_fast_equals_exact_adversarial_grids(gpu, case):
+    """Grids that make certification hard or impossible (very dense cells,
+    one-point layers, near-duplicate points -> x_safe tiny or 0, points far
+    apart) must still give the exact kernel's counts."""
+    from paper_1101_3228_b200.device import Plan
+    q = Q()
+    n = 12
+    ch = q.BrownianChain1d(n)
+    rng = np.random.default_rng(7)
+    grids = []
+    for k in range(1, n + 1):
+        if case == "dense":
+            pts = np.sort(rng.standard_normal(2000)) * np.sqrt(k / n)
+        elif case == "single":
+            pts = np.array([0.1 * k]) if k % 2 else np.array([-1.0, 1.0])
+        elif case == "tiny_gap":
+            base = rng.standard_normal(64)
+            pts = np.concatenate([base, base + 1e-13])
+        else:
+            pts = rng.standard_normal(100) * 1e6
+        grids.append(q.QuantGrid(1, pts))
+    plan = Plan(ch, grids, 0)
+    assert np.array_equal(_counts(plan, 100000, 0, 10**7, True),
+                          _counts(plan, 100000, 0, 10**7, False)), case
+
+
+def test_fast_window_vs_oracle(gpu, oracle):
+    q = Q()
+    ch = q.BrownianChain1d(50)
+    grids = q.build_brownian_grids(ch, 500)
+    spec = ChainSpec(CHAIN_BROWNIAN1D, 50)
+    sizes = np.array([1] + [500] * 50, np.uint64)
+    pts = np.concatenate([g.data() for g in grids])
+    first = 314159265
+    v, j = q.accumulate_paths(ch, grids, 1, 12345, first, 40000, 10**9)
+    rv, rj = oracle.accumulate_paths(spec, sizes, pts, 1, 12345, first, 40000, 10**9)
+    assert np.array_equal(v, rv) and np.array_equal(j, rj)
+    st = q.fast_stats()
+    assert st["fast_paths"] >= 40000
