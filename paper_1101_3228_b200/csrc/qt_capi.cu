@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -115,6 +116,52 @@ std::vector<uint32_t> mrg_jump_table() {
     c2 = mat_mul(c2, c2, kM2);
   }
   return t;
+}
+
+uint64_t powmod(uint64_t b, uint64_t e, uint64_t m) {
+  uint64_t r = 1;
+  b %= m;
+  for (; e; e >>= 1) {
+    if (e & 1) r = static_cast<uint64_t>(static_cast<u128>(r) * b % m);
+    b = static_cast<uint64_t>(static_cast<u128>(b) * b % m);
+  }
+  return r;
+}
+
+// (J^e)^-1 mod m (m prime) by the adjugate
+Mat3 mat_pow_inv(Mat3 c, uint64_t e, uint64_t m) {
+  Mat3 r{{{1, 0, 0}, {0, 1, 0}, {0, 0, 1}}};
+  for (; e; e >>= 1) {
+    if (e & 1) r = mat_mul(r, c, m);
+    c = mat_mul(c, c, m);
+  }
+  auto mm = [&](uint64_t x, uint64_t y) { return static_cast<uint64_t>(static_cast<u128>(x) * y % m); };
+  auto sub = [&](uint64_t x, uint64_t y) { return (x + m - y) % m; };
+  Mat3 adj{};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      // cofactor of (j, i)
+      const int r0 = (j + 1) % 3, r1 = (j + 2) % 3, c0 = (i + 1) % 3, c1 = (i + 2) % 3;
+      adj.a[i][j] = sub(mm(r.a[r0][c0], r.a[r1][c1]), mm(r.a[r0][c1], r.a[r1][c0]));
+    }
+  uint64_t det = 0;
+  for (int k = 0; k < 3; ++k) det = (det + mm(r.a[0][k], adj.a[k][0])) % m;
+  const uint64_t inv = powmod(det, m - 2, m);
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) adj.a[i][j] = mm(adj.a[i][j], inv);
+  return adj;
+}
+
+// MRG32k3a state <- (J^D)^-1 state: from the end of a path back to its start
+void mrg_back_jump(uint64_t D, uint32_t out[18]) {
+  const Mat3 c1{{{0, 1, 0}, {0, 0, 1}, {kM1 - 810728ull, 1403580ull, 0}}};
+  const Mat3 c2{{{0, 1, 0}, {0, 0, 1}, {kM2 - 1370589ull, 0, 527612ull}}};
+  const Mat3 i1 = mat_pow_inv(c1, D, kM1), i2 = mat_pow_inv(c2, D, kM2);
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      out[3 * i + j] = static_cast<uint32_t>(i1.a[i][j]);
+      out[9 + 3 * i + j] = static_cast<uint32_t>(i2.a[i][j]);
+    }
 }
 
 constexpr uint64_t kLcgMask = (1ull << 48) - 1;
@@ -375,32 +422,51 @@ std::vector<uint8_t> build_fast_table(int kind, const std::vector<double>& t,
   h.fs = f32_up_abs(kind == QT_CHAIN_OU_1D ? step[2] : step[0]);
   h.x_safe = x_safe > 0.0 ? std::max(0.0f, f32_down(x_safe)) : 0.0f;
   h.n_pts = static_cast<uint32_t>(N);
-  // uniform FP32 bucket map over [t_0, t_{N-2}]: the fewest buckets (multiple
-  // of N, <= 8N) that hold at most one threshold each
+  // bucket map over g(t_0) .. g(t_{N-2}), g(x) = x / sqrt(1 + gc x^2): the
+  // fewest buckets (over a few gc) that hold at most one threshold each
   uint32_t nb = 1;
-  float bk_a = 0.0f, bk_b = 0.0f;
-  const double span = N > 2 ? t[N - 2] - t[0] : 0.0;
-  if (N > 2 && span > 0.0 && std::isfinite(span)) {
-    for (uint32_t m = 1; m <= 8; ++m) {
-      const uint32_t cand = static_cast<uint32_t>(m * N);
-      const float a = static_cast<float>(cand / span);
-      const float b = static_cast<float>(-t[0] * (cand / span));
-      if (!std::isfinite(a) || !std::isfinite(b)) break;
-      uint32_t prev = 0xFFFFFFFFu, run = 0, worst = 0;
-      for (uint64_t c = 0; c + 1 < N; ++c) {
-        const uint32_t bb = qt::fbucket(static_cast<float>(t[c]), a, b, cand - 1);
-        run = bb == prev ? run + 1 : 1;
-        prev = bb;
-        worst = std::max(worst, run);
+  double bk_a = 0.0, bk_b = 0.0, gc = 0.0;
+  if (N > 2 && std::isfinite(t[0]) && std::isfinite(t[N - 2]) && t[N - 2] > t[0]) {
+    std::vector<double> mags;
+    for (uint64_t c = 0; c + 1 < N; ++c) mags.push_back(std::fabs(t[c]));
+    std::nth_element(mags.begin(), mags.begin() + mags.size() / 2, mags.end());
+    const double scale = std::max(mags[mags.size() / 2] / 0.6745, 1e-300);  // ~ sd of the cells
+    uint32_t best = 0;
+    for (double q : {0.0, 0.03, 0.06, 0.1, 0.15, 0.22, 0.3}) {
+      const double g = q / (scale * scale);
+      const double u0 = qt::fmap_g(t[0], g), u1 = qt::fmap_g(t[N - 2], g);
+      if (!(u1 > u0) || !std::isfinite(u1 - u0)) continue;
+      for (uint32_t m4 = 4; m4 <= 32; ++m4) {  // nb = m4/4 N
+        const uint32_t cand = static_cast<uint32_t>((static_cast<uint64_t>(m4) * N + 3) / 4);
+        if (best && cand >= best) break;
+        const double a = cand / (u1 - u0), bb = -u0 * a;
+        uint32_t prev = 0xFFFFFFFFu, worst = 0, run = 0;
+        for (uint64_t c = 0; c + 1 < N; ++c) {
+          const uint32_t b = qt::fbucket_host(t[c], g, a, bb, cand - 1);
+          run = b == prev ? run + 1 : 1;
+          prev = b;
+          worst = std::max(worst, run);
+        }
+        if (worst <= 1) {
+          best = cand;
+          nb = cand;
+          bk_a = a;
+          bk_b = bb;
+          gc = g;
+          break;
+        }
       }
-      nb = cand;
-      bk_a = a;
-      bk_b = b;
-      if (worst <= 1) break;
+    }
+    if (!best) {  // no map found: uniform, 8N (records still certify correctly)
+      nb = static_cast<uint32_t>(8 * N);
+      bk_a = nb / (t[N - 2] - t[0]);
+      bk_b = -t[0] * bk_a;
+      gc = 0.0;
     }
   }
-  h.bk_a = bk_a;
-  h.bk_b = bk_b;
+  h.bk_a = static_cast<float>(bk_a);
+  h.bk_b = static_cast<float>(bk_b);
+  h.gc = static_cast<float>(gc);
   h.nb1 = nb - 1;
   h.bytes = round16(sizeof(qt::FastHdr) + 16ull * nb);
   std::vector<uint8_t> out(h.bytes, 0);
@@ -409,7 +475,7 @@ std::vector<uint8_t> build_fast_table(int kind, const std::vector<double>& t,
   const float inf = std::numeric_limits<float>::infinity();
   uint64_t c = 0;
   for (uint32_t b = 0; b < nb; ++b) {
-    while (c + 1 < N && qt::fbucket(static_cast<float>(t[c]), bk_a, bk_b, nb - 1) < b) ++c;
+    while (c + 1 < N && qt::fbucket_host(t[c], gc, bk_a, bk_b, nb - 1) < b) ++c;
     qt::FRec r;
     r.tl = c ? f32_up(t[c - 1]) : -inf;
     r.t0 = f32_down(t[c]);
@@ -568,7 +634,7 @@ struct qt_plan {
   uint64_t* d_fin = nullptr;  // rows, cols, joff, voff_row, voff_col (5 x n)
   std::vector<uint8_t> host_tables;
   // fast 1-D path: replay list + counters (FastArgs::stats), paths sent to it
-  unsigned long long* d_amb = nullptr;
+  qt::AmbEntry* d_amb = nullptr;
   unsigned long long* d_stats = nullptr;
   uint8_t* d_ftables = nullptr;  // fast-path tables (d == 1), concatenated
   uint32_t* d_ftab_off = nullptr;
@@ -667,6 +733,8 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
       ftables.insert(ftables.end(), b.fast.begin(), b.fast.end());
     }
     p->total_ftab = static_cast<uint32_t>(ftables.size());
+    if (std::getenv("QT_DEBUG"))
+      std::fprintf(stderr, "qtree: fast tables max %u B, total %u B\n", p->max_ftab, p->total_ftab);
   }
   // cold blocks after all hot tables; patch each header's cold_off
   for (int k = 1; k <= n; ++k) {
@@ -761,23 +829,18 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
         QT_CUDA(cudaFree(p->d_amb));
         p->d_amb = nullptr;
         p->amb_cap = 0;
-        QT_CUDA(cudaMalloc(&p->d_amb, want * sizeof(unsigned long long)));
+        QT_CUDA(cudaMalloc(&p->d_amb, want * sizeof(qt::AmbEntry)));
         p->amb_cap = want;
       }
-      int P = 2;
-      if (const char* e = std::getenv("QT_FAST_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 4 ? 4 : 2;
-      // fast tables staged by the ring (all resident when they fit)
+      int P = 4;  // paths in flight per thread (QT_FAST_P = 1 / 2 / 4)
+      if (const char* e = std::getenv("QT_FAST_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 2 ? 2 : 4;
+      // fast tables: all resident when they fit, else prefetched S layers ahead
       const bool fres = p->total_ftab <= kResidentBudget;
-      size_t fsmem = fres ? p->total_ftab : static_cast<size_t>(2) * p->max_ftab;
+      uint32_t st_n = 3;
+      if (const char* e = std::getenv("QT_FAST_STAGES")) st_n = std::max(2, std::min(8, std::atoi(e)));
+      const size_t fsmem = fres ? p->total_ftab : static_cast<size_t>(st_n) * p->max_ftab;
       qt::PathArgs fa_args = a;
-      int bps = qt::paths_fast_blocks_per_sm(p->kind, fres, P, fsmem);
-      uint32_t st_n = 2;
-      if (!fres) {  // ring depth: as many stages as the resident CTAs leave room for
-        const uint32_t per_cta = (200u * 1024u) / static_cast<uint32_t>(bps);
-        st_n = std::max<uint32_t>(2, std::min<uint32_t>(8, per_cta / std::max(p->max_ftab, 1u)));
-        fsmem = static_cast<size_t>(st_n) * p->max_ftab;
-        bps = qt::paths_fast_blocks_per_sm(p->kind, fres, P, fsmem);
-      }
+      const int bps = qt::paths_fast_blocks_per_sm(p->kind, fres, P, fsmem);
       uint64_t blocks = static_cast<uint64_t>(p->sm_count) * bps;
       const uint64_t slots_per_block = static_cast<uint64_t>(qt::kPathConsumers) * P;
       const uint64_t need = (count + slots_per_block - 1) / slots_per_block;
@@ -787,7 +850,8 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       fa_args.rem = count % T;
       qt::FastArgs fa{fa_args, p->d_amb, p->d_stats, std::min(p->amb_cap, want),
                       p->d_ftables, p->d_ftab_off, p->d_ftab_bytes, p->max_ftab, p->total_ftab,
-                      st_n};
+                      st_n, {}, std::getenv("QT_PROBE_NORED") ? 1u : 0u};
+      mrg_back_jump(2 * ((static_cast<uint64_t>(p->n) + 1) / 2), fa.back);
       QT_CUDA(cudaMemsetAsync(p->d_stats, 0, sizeof(unsigned long long), st));
       QT_CUDA(qt::launch_paths_fast(p->kind, fres, P, fa, static_cast<uint32_t>(blocks), fsmem,
                                     static_cast<uint32_t>(p->sm_count) * 4u, st));

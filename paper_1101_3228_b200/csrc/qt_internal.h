@@ -41,9 +41,15 @@ struct PathArgs {
 constexpr int kPathConsumers = 256;  // consumer threads per k_paths CTA
 
 // Fast 1-D path (FP32 Box-Muller with certified cells + exact replay).
+struct AmbEntry {
+  unsigned long long key;  // (path << 16) | first uncertified layer
+  uint32_t st[6];          // MRG32k3a state at the path's first draw
+};
+static_assert(sizeof(AmbEntry) == 32, "AmbEntry is 32 bytes");
+
 struct FastArgs {
   PathArgs p;
-  unsigned long long* amb;    // ambiguous paths: (path << 16) | first uncertified layer
+  AmbEntry* amb;              // ambiguous paths
   unsigned long long* stats;  // [0] entries of this launch, [1] replayed (cumulative),
                               // [2] replayed inline on list overflow (cumulative)
   uint64_t cap;               // capacity of amb
@@ -52,7 +58,9 @@ struct FastArgs {
   const uint32_t* ftab_bytes; // [n]
   uint32_t fbuf_bytes;        // ring stage size (max fast table)
   uint32_t fresident_bytes;   // sum of fast tables (resident mode)
-  uint32_t fstages;           // ring depth
+  uint32_t fstages;           // prefetch depth (stages of fbuf_bytes)
+  uint32_t back[18];          // (J^D)^-1 mod m1 | mod m2: path end -> path start
+  uint32_t probe_nored;       // diagnostics only (QT_PROBE_NORED): skip the count REDs
 };
 
 struct Alg3Args {

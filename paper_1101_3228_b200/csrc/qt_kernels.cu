@@ -34,6 +34,7 @@ constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kPathThreads = kConsumers + 32;
 constexpr int kMaxStages = 8;
+constexpr int kFastThreads = 256;  // k_paths_fast: 8 warps in layer lockstep
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -145,28 +146,6 @@ __global__ void __launch_bounds__(kPathThreads) k_paths(const PathArgs a) {
 // from that layer on. The counts are therefore identical to k_paths' counts.
 // ---------------------------------------------------------------------------
 
-// Exact FP64 recomputation of path `path` (the body of k_paths, tables read
-// from global memory), counting transitions k >= k0.
-template <int K>
-__device__ __noinline__ void replay_path(const PathArgs& a, uint64_t path, uint32_t k0) {
-  using C = Chain<K>;
-  Source<kSrcMrg> src;
-  src.start(a.src, path);
-  double x[1] = {0.0};
-  uint32_t i = 0;
-  for (uint32_t k = 1; k <= a.n; ++k) {
-    const uint8_t* tb = a.tables + __ldg(a.tab_off + k - 1);
-    const LayerTable& h = *reinterpret_cast<const LayerTable*>(tb);
-    double e[1], xn[1];
-    e[0] = src.normal();
-    C::step(h.step, x, xn, e);
-    x[0] = xn[0];
-    const uint32_t j = nearest_1d(h, tb, x[0], a.tables);
-    if (k >= k0) red_add_u64(a.joint + h.joff + static_cast<uint64_t>(i) * h.n_pts + j, 1ull);
-    i = j;
-  }
-}
-
 // Per-slot state of the fast kernel (one path in flight).
 struct FastPath {
   Mrg st;
@@ -187,11 +166,11 @@ struct FastPath {
 template <int K, int P>
 __device__ __forceinline__ void fast_layer(FastPath (&ps)[P], const bool (&act)[P],
                                            const uint8_t* tb, uint32_t k,
-                                           unsigned long long* joint) {
+                                           unsigned long long* joint, bool count) {
   const FastHdr& h = *reinterpret_cast<const FastHdr*>(tb);
   const double c0 = h.c0;
   const double c2 = K == 0 ? 0.0 : h.c2;
-  const float fa = h.fa, fs = h.fs, bk_a = h.bk_a, bk_b = h.bk_b, x_safe = h.x_safe;
+  const float fa = h.fa, fs = h.fs, bk_a = h.bk_a, bk_b = h.bk_b, x_safe = h.x_safe, gc = h.gc;
   const uint32_t nb1 = h.nb1, npts = h.n_pts;
   const FRec* R = reinterpret_cast<const FRec*>(tb + sizeof(FastHdr));
   unsigned long long* jl = joint + h.joff;
@@ -233,7 +212,7 @@ __device__ __forceinline__ void fast_layer(FastPath (&ps)[P], const bool (&act)[
                                                                             fabsf(ps[p].xs)))));
     ps[p].x = xn;
     ps[p].xs = xns;
-    rec[p] = R[fbucket(xns, bk_a, bk_b, nb1)];
+    rec[p] = R[fbucket(xns, gc, bk_a, bk_b, nb1)];
   }
 #pragma unroll
   for (int p = 0; p < P; ++p) {
@@ -249,61 +228,86 @@ __device__ __forceinline__ void fast_layer(FastPath (&ps)[P], const bool (&act)[
     const uint32_t cell = lo ? r.o0 : r.o1;
     const bool ok = xl >= lb && xh < ub && __fadd_ru(fabsf(xs), E) < x_safe;
     const bool live = act[p] && ps[p].amb_k == 0;
-    if (live && ok) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + cell, 1ull);
+    if (live && ok && count) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + cell, 1ull);
     ps[p].i = cell;
     if (live && !ok) ps[p].amb_k = k;
   }
 }
 
+// Replay of an ambiguous path from its stored start state (no jump-ahead).
+template <int K>
+__device__ __noinline__ void replay_entry(const PathArgs& a, const AmbEntry& ent) {
+  using C = Chain<K>;
+  Source<kSrcMrg> src;
+  src.s = Mrg{ent.st[0], ent.st[1], ent.st[2], ent.st[3], ent.st[4], ent.st[5]};
+  src.has = false;
+  const uint32_t k0 = static_cast<uint32_t>(ent.key & 0xFFFFu);
+  double x[1] = {0.0};
+  uint32_t i = 0;
+  for (uint32_t k = 1; k <= a.n; ++k) {
+    const uint8_t* tb = a.tables + __ldg(a.tab_off + k - 1);
+    const LayerTable& h = *reinterpret_cast<const LayerTable*>(tb);
+    double e[1], xn[1];
+    e[0] = src.normal();
+    C::step(h.step, x, xn, e);
+    x[0] = xn[0];
+    const uint32_t j = nearest_1d(h, tb, x[0], a.tables);
+    if (k >= k0) red_add_u64(a.joint + h.joff + static_cast<uint64_t>(i) * h.n_pts + j, 1ull);
+    i = j;
+  }
+}
+
+// state <- M state with M = 18 residues in generic (param-space) memory
+__device__ __forceinline__ void mrg_apply(const uint32_t* M, Mrg& s) {
+  uint32_t r[6];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    r[i] = red_m1(static_cast<uint64_t>(red_m1(mulw(M[3 * i], s.a0))) + red_m1(mulw(M[3 * i + 1], s.a1)) +
+                  red_m1(mulw(M[3 * i + 2], s.a2)));
+    r[3 + i] = red_m2(static_cast<uint64_t>(red_m2(mulw(M[9 + 3 * i], s.b0))) +
+                      red_m2(mulw(M[9 + 3 * i + 1], s.b1)) + red_m2(mulw(M[9 + 3 * i + 2], s.b2)));
+  }
+  s = Mrg{r[0], r[1], r[2], r[3], r[4], r[5]};
+}
+
+// The fast path kernel. All 256 threads of a CTA walk the layers in lockstep
+// (one named barrier per layer); thread 0 keeps the next fstages - 1 layer
+// tables in flight with cp.async.bulk, each stage reused only after the
+// barrier that ends its layer. Slot v = gid P + p owns a contiguous run of
+// paths, so its MRG32k3a stream flows from path to path without jumps.
 template <int K, bool RESIDENT, int P>
-__global__ void __launch_bounds__(kPathThreads) k_paths_fast(const __grid_constant__ FastArgs f) {
+__global__ void __launch_bounds__(kFastThreads) k_paths_fast(const __grid_constant__ FastArgs f) {
   const PathArgs& a = f.p;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
-  __shared__ __align__(8) uint64_t empty[kMaxStages];
-  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+  const uint32_t tid = threadIdx.x;
   const uint32_t S = f.fstages;
   const uint64_t rounds = a.q + (a.rem ? 1u : 0u);
   const uint64_t steps_total = rounds * a.n;
   if (steps_total == 0) return;
 
+  // issue the table of global layer step g into its stage (thread 0 only)
+  auto issue = [&](uint64_t g) {
+    const uint32_t k = static_cast<uint32_t>(g % a.n);
+    const uint32_t st = static_cast<uint32_t>(g % S);
+    const uint32_t bytes = __ldg(f.ftab_bytes + k);
+    mbar_expect_tx(&full[st], bytes);
+    bulk_g2s(smem + st * f.fbuf_bytes, f.ftables + __ldg(f.ftab_off + k), bytes, &full[st]);
+  };
   if (tid == 0) {
-    for (uint32_t s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
-    }
+    for (uint32_t s = 0; s < S; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
+    if constexpr (RESIDENT) {
+      mbar_expect_tx(&full[0], f.fresident_bytes);
+      for (uint32_t k = 0; k < a.n; ++k)
+        bulk_g2s(smem + f.ftab_off[k], f.ftables + f.ftab_off[k], f.ftab_bytes[k], &full[0]);
+    } else {
+      for (uint64_t g = 0; g < S && g < steps_total; ++g) issue(g);
+    }
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {  // ---- producer warp (as k_paths) ----
-    if (lane == 0) {
-      if constexpr (RESIDENT) {
-        mbar_expect_tx(&full[0], f.fresident_bytes);
-        for (uint32_t k = 0; k < a.n; ++k)
-          bulk_g2s(smem + f.ftab_off[k], f.ftables + f.ftab_off[k], f.ftab_bytes[k], &full[0]);
-      } else {
-        uint32_t k = 0, s = 0, ph = 0;
-        for (uint64_t g = 0; g < steps_total; ++g) {
-          mbar_wait(&empty[s], ph ^ 1u);
-          const uint32_t bytes = __ldg(f.ftab_bytes + k);
-          mbar_expect_tx(&full[s], bytes);
-          bulk_g2s(smem + s * f.fbuf_bytes, f.ftables + __ldg(f.ftab_off + k), bytes, &full[s]);
-          k = k + 1 == a.n ? 0 : k + 1;
-          if (++s == S) {
-            s = 0;
-            ph ^= 1u;
-          }
-        }
-      }
-    }
-    return;
-  }
-
-  // P slots per consumer thread: slot v = gid P + p owns a contiguous run of
-  // paths (the window split over T P slots), so each slot's stream flows from
-  // path to path without jumps; the P slots share the layer wait.
-  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * kConsumers + tid;
+  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * kFastThreads + tid;
   FastPath ps[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
@@ -318,8 +322,9 @@ __global__ void __launch_bounds__(kPathThreads) k_paths_fast(const __grid_consta
     }
   }
   if constexpr (RESIDENT) mbar_wait(&full[0], 0);
-  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
+  const uint32_t full0 = smem_u32(full);
   uint32_t s = 0, ph = 0;
+  uint64_t g = 0;
   const uint8_t* tb = smem;
   for (uint64_t r = 0; r < rounds; ++r) {
     bool act[P];
@@ -332,16 +337,16 @@ __global__ void __launch_bounds__(kPathThreads) k_paths_fast(const __grid_consta
       ps[p].i = 0;
       ps[p].amb_k = 0;
     }
-    for (uint32_t k = 1; k <= a.n; ++k) {
+    for (uint32_t k = 1; k <= a.n; ++k, ++g) {
       if constexpr (RESIDENT) {
         tb = smem + f.ftab_off[k - 1];
       } else {
         mbar_wait_u32(full0 + 8u * s, ph);
       }
-      fast_layer<K, P>(ps, act, tb, k, a.joint);
+      fast_layer<K, P>(ps, act, tb, k, a.joint, f.probe_nored == 0);
       if constexpr (!RESIDENT) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive_u32(empty0 + 8u * s);
+        named_barrier_sync(1, kFastThreads);  // every thread is done with stage s
+        if (tid == 0 && g + S < steps_total) issue(g + S);
         tb += f.fbuf_bytes;
         if (++s == S) {
           s = 0;
@@ -353,12 +358,21 @@ __global__ void __launch_bounds__(kPathThreads) k_paths_fast(const __grid_consta
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       if (act[p] && ps[p].amb_k != 0) {
-        const uint64_t path = ps[p].beg + r;
+        AmbEntry ent;
+        ent.key = ((ps[p].beg + r) << 16) | ps[p].amb_k;
+        Mrg st0 = ps[p].st;
+        mrg_apply(f.back, st0);  // the path's start state
+        ent.st[0] = st0.a0;
+        ent.st[1] = st0.a1;
+        ent.st[2] = st0.a2;
+        ent.st[3] = st0.b0;
+        ent.st[4] = st0.b1;
+        ent.st[5] = st0.b2;
         const unsigned long long idx = atomicAdd(f.stats, 1ull);
         if (idx < f.cap) {
-          f.amb[idx] = (path << 16) | ps[p].amb_k;
+          f.amb[idx] = ent;
         } else {  // list full: replay here (correct, slow; never expected)
-          replay_path<K>(a, path, ps[p].amb_k);
+          replay_entry<K>(a, ent);
           atomicAdd(f.stats + 2, 1ull);
         }
       }
@@ -373,10 +387,8 @@ __global__ void __launch_bounds__(256) k_replay(const __grid_constant__ FastArgs
   const uint64_t n = entries < f.cap ? entries : f.cap;
   const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g0 == 0) atomicAdd(f.stats + 1, static_cast<unsigned long long>(n));
-  for (uint64_t g = g0; g < n; g += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const unsigned long long ent = f.amb[g];
-    replay_path<K>(f.p, ent >> 16, static_cast<uint32_t>(ent & 0xFFFFu));
-  }
+  for (uint64_t g = g0; g < n; g += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    replay_entry<K>(f.p, f.amb[g]);
 }
 
 // Exhaustive check of the FP32 Box-Muller bounds over all 2^32 - 209 MRG32k3a
@@ -653,9 +665,10 @@ static cudaError_t launch_fast_t(const FastArgs& a, dim3 grid, size_t smem, uint
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  fn<<<grid, kPathThreads, smem, st>>>(a);
+  fn<<<grid, kFastThreads, smem, st>>>(a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   k_replay<K><<<rblocks, 256, 0, st>>>(a);
+
   return cudaGetLastError();
 }
 
@@ -692,7 +705,7 @@ int paths_fast_blocks_per_sm(int kind, bool resident, int P, size_t smem) {
   else fn = P == 1 ? fast_fn<2, 1>(resident) : P == 4 ? fast_fn<2, 4>(resident) : fast_fn<2, 2>(resident);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kPathThreads, smem) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kFastThreads, smem) != cudaSuccess)
     return 1;
   return nb > 0 ? nb : 1;
 }

@@ -21,9 +21,8 @@
 // CTA that holds a layer's table in shared memory has everything one step needs.
 #pragma once
 #include <stdint.h>
-#if !defined(__CUDA_ARCH__)
+
 #include <cmath>
-#endif
 
 namespace qt {
 
@@ -68,15 +67,18 @@ static_assert(sizeof(Rec1) == 16, "Rec1 is 16 bytes");
 
 // ---------------------------------------------------------------------------
 // Fast-path layer table (d == 1 only; k_paths_fast). One 16-byte record per
-// bucket of an FP32 bucket map b(x) = min(u32_rz(fmaf(fl32(x), bk_a, bk_b)),
-// nb - 1), the SAME IEEE operations on host and device. With c = #{thresholds
-// t whose b(t) < b} (monotonicity of b gives t_{c-1} < x for every x in bucket
-// b), the record holds the thresholds around c rounded OUTWARD to FP32 and the
-// original indices of cells c and c + 1, so one 16-byte shared-memory load
-// decides and certifies a transition:
+// bucket of an FP32 bucket map b(x) = min(u32_rz(fmaf(g(x), bk_a, bk_b)),
+// nb - 1) over the density-equalising coordinate g(x) = x / sqrt(1 + gc x^2)
+// (the Lloyd cells are ~5x narrower at the centre than in the tails). With
+// c = #{thresholds t whose b(t) < b}, the record holds the thresholds around
+// c rounded OUTWARD to FP32 and the original indices of cells c and c + 1, so
+// one 16-byte shared-memory load decides and certifies a transition:
 //   x in [xl, xh], xh < t0      and xl >= tl      -> cell o0
 //   x in [xl, xh], xh < t1      and xl >= up(t0)  -> cell o1
-// (any other case is left uncertified -> exact replay).
+// Any other case is left uncertified (-> exact replay). The record carries the
+// bounds of the cell it certifies, so correctness never depends on the bucket
+// map: the device's approximate g (MUFU rsqrt) may differ from the host's at
+// bucket edges, which only costs a (vanishingly rare) replay.
 // ---------------------------------------------------------------------------
 struct alignas(16) FastHdr {
   double c0, c2;      // step coefficients: Brownian x + c0 eps; OU c0 x + c2 eps
@@ -87,6 +89,8 @@ struct alignas(16) FastHdr {
   uint32_t nb1;       // buckets - 1
   uint32_t n_pts;     // N_k
   uint32_t bytes;     // table bytes (multiple of 16)
+  float gc;           // density-equalising map u = x / sqrt(1 + gc x^2) before bucketing
+  uint32_t pad_;
 };
 static_assert(sizeof(FastHdr) == 64, "FastHdr is 64 bytes");
 
@@ -98,17 +102,20 @@ struct alignas(16) FRec {
 };
 static_assert(sizeof(FRec) == 16, "FRec is 16 bytes");
 
-// The FP32 bucket map shared by host (table build) and device (query).
+// The bucket map: host (table build, FP64) and device (query, FP32 + MUFU).
 #if defined(__CUDACC__)
-__host__ __device__
+__device__ __forceinline__ uint32_t fbucket(float xs, float gc, float bk_a, float bk_b,
+                                            uint32_t nb1) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__fmaf_rn(gc, __fmul_rn(xs, xs), 1.0f)));
+  const uint32_t b = __float2uint_rz(__fmaf_rn(__fmul_rn(xs, r), bk_a, bk_b));
+  return b < nb1 ? b : nb1;
+}
 #endif
-inline uint32_t fbucket(float xs, float bk_a, float bk_b, uint32_t nb1) {
-#if defined(__CUDA_ARCH__)
-  const uint32_t b = __float2uint_rz(__fmaf_rn(xs, bk_a, bk_b));
-#else
-  const float v = std::fmaf(xs, bk_a, bk_b);
-  const uint32_t b = !(v > 0.0f) ? 0u : (v >= 4294967296.0f ? 0xFFFFFFFFu : static_cast<uint32_t>(v));
-#endif
+inline double fmap_g(double x, double gc) { return x / std::sqrt(1.0 + gc * x * x); }
+inline uint32_t fbucket_host(double x, double gc, double bk_a, double bk_b, uint32_t nb1) {
+  const double v = fmap_g(x, gc) * bk_a + bk_b;
+  const uint32_t b = !(v > 0.0) ? 0u : (v >= 4294967295.0 ? 0xFFFFFFFFu : static_cast<uint32_t>(v));
   return b < nb1 ? b : nb1;
 }
 
