@@ -44,7 +44,7 @@ CONFIGS = {
     "c2": ("C2: 1-D Black-Scholes American put, n=50, N=500, M=1e9 paths", "bm", 50, 500, 10**9, 1),
     "c3": ("C3: 1-D OU swing, Alg III pair sampling, n=365, N=200, M=1e7 per layer", "ou", 365, 200,
            10**7, 2),
-    "c4": ("C4: 2-factor AR(1) gas swing, n=365, N=1000, M=1e6 paths", "tf", 365, 1000, 10**6, 1),
+    "c4": ("C4: 2-factor AR(1) gas swing, n=365, N=1000, M=1e7 paths", "tf", 365, 1000, 10**7, 1),
     "c5": ("C5: 3-D GBM max-call, n=20, N=4000, M=1e6 paths", "gbm", 20, 4000, 10**6, 1),
 }
 

@@ -39,6 +39,12 @@ std::atomic<int> g_fast{-1};
 // cumulative fast-path evidence of destroyed plans: paths, replayed, inline-replayed
 std::atomic<uint64_t> g_fast_paths{0}, g_fast_replayed{0}, g_fast_inline{0};
 
+// d >= 2 FP32-scan kernel: enabled unless QT_SCAN=0
+bool scan_enabled() {
+  const char* e = std::getenv("QT_SCAN");
+  return !(e && e[0] == '0');
+}
+
 bool fast_enabled() {
   int v = g_fast.load();
   if (v < 0) {
@@ -489,6 +495,56 @@ std::vector<uint8_t> build_fast_table(int kind, const std::vector<double>& t,
 
 // One layer's table (layout in qt_layout.h). header.cold_off is patched by
 // the caller once the cold block's position is known.
+// FP32 scan table of one d >= 2 layer (ScanHdr + paired FP32 points), qt_layout.h
+std::vector<uint8_t> build_scan_table(int dim, uint64_t N, const double* pts, const double* step,
+                                      uint64_t joff, uint64_t exact_off) {
+  qt::ScanHdr h{};
+  std::memcpy(h.step, step, sizeof h.step);
+  h.joff = joff;
+  h.exact_off = exact_off;
+  h.n_pts = static_cast<uint32_t>(N);
+  h.n_chunks = static_cast<uint32_t>((N + 2 * qt::kScanChunkPairs - 1) / (2 * qt::kScanChunkPairs));
+  const uint64_t npairs = static_cast<uint64_t>(h.n_chunks) * qt::kScanChunkPairs;
+  h.off_b = static_cast<uint32_t>(sizeof(qt::ScanHdr) + 16 * npairs);
+  h.bytes = round16(h.off_b + (dim == 2 ? 8 : 16) * npairs);
+  std::vector<uint8_t> out(h.bytes, 0);
+  float* XY = reinterpret_cast<float*>(out.data() + sizeof(qt::ScanHdr));
+  float* B = reinterpret_cast<float*>(out.data() + h.off_b);
+  const float inf = std::numeric_limits<float>::infinity();
+  double hmax = 0.0, pmax[3] = {0.0, 0.0, 0.0};
+  bool ok = true;
+  for (uint64_t idx = 0; idx < 2 * npairs; ++idx) {
+    const uint64_t pr = idx / 2, ln = idx % 2;
+    if (idx < N) {
+      const double* pp = pts + idx * dim;
+      double hh = 0.0;
+      for (int c = 0; c < dim; ++c) {
+        hh += pp[c] * pp[c];
+        pmax[c] = std::max(pmax[c], std::fabs(pp[c]));
+        ok = ok && std::fabs(pp[c]) < 0x1p40;
+      }
+      hh *= 0.5;
+      hmax = std::max(hmax, hh);
+      XY[4 * pr + ln] = static_cast<float>(pp[0]);
+      XY[4 * pr + 2 + ln] = static_cast<float>(pp[1]);
+      if (dim == 2) {
+        B[2 * pr + ln] = static_cast<float>(hh);
+      } else {
+        B[4 * pr + ln] = static_cast<float>(pp[2]);
+        B[4 * pr + 2 + ln] = static_cast<float>(hh);
+      }
+    } else {  // padding: p = 0, h = +inf (never a candidate)
+      if (dim == 2) B[2 * pr + ln] = inf;
+      else B[4 * pr + 2 + ln] = inf;
+    }
+  }
+  h.hmax = f32_up(hmax * (1.0 + 0x1p-50));
+  for (int c = 0; c < dim; ++c) h.pmax[c] = f32_up(pmax[c]);
+  h.fp32_ok = ok && std::isfinite(h.hmax) ? 1u : 0u;
+  std::memcpy(out.data(), &h, sizeof h);
+  return out;
+}
+
 TableBlob build_table(int kind, int dim, uint64_t npts, const double* pts, const double* step,
                       const double* marg_prev, uint64_t joff, uint64_t n_prev, uint32_t layer) {
   LayerTable h{};
@@ -636,6 +692,10 @@ struct qt_plan {
   // fast 1-D path: replay list + counters (FastArgs::stats), paths sent to it
   qt::AmbEntry* d_amb = nullptr;
   unsigned long long* d_stats = nullptr;
+  uint8_t* d_stables = nullptr;  // FP32 scan tables (d >= 2), concatenated
+  uint32_t* d_stab_off = nullptr;
+  uint32_t* d_stab_bytes = nullptr;
+  uint32_t max_stab = 0, total_stab = 0;
   uint8_t* d_ftables = nullptr;  // fast-path tables (d == 1), concatenated
   uint32_t* d_ftab_off = nullptr;
   uint32_t* d_ftab_bytes = nullptr;
@@ -655,6 +715,9 @@ struct qt_plan {
     cudaFree(d_amb);
     cudaFree(d_stats);
     cudaFree(d_ftables);
+    cudaFree(d_stables);
+    cudaFree(d_stab_off);
+    cudaFree(d_stab_bytes);
     cudaFree(d_ftab_off);
     cudaFree(d_ftab_bytes);
     cudaFree(d_tables);
@@ -748,11 +811,36 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
     p->host_tables.insert(p->host_tables.end(), b.cold.begin(), b.cold.end());
   }
   p->stages = std::max<uint32_t>(2, std::min<uint32_t>(8, kStageBudget / std::max(p->max_tab, 1u)));
+  // FP32 scan tables (d >= 2)
+  std::vector<uint8_t> stables;
+  std::vector<uint32_t> soff, sbytes;
+  if (p->dim >= 2) {
+    const double* sp = grids->points;
+    for (int k = 1; k <= n; ++k) {
+      const uint64_t N = p->sizes[k];
+      auto t = build_scan_table(p->dim, N, sp, chain->step + 6 * (k - 1), p->joff[k - 1],
+                                p->tab_off[k - 1]);
+      soff.push_back(static_cast<uint32_t>(stables.size()));
+      sbytes.push_back(static_cast<uint32_t>(t.size()));
+      p->max_stab = std::max<uint32_t>(p->max_stab, static_cast<uint32_t>(t.size()));
+      stables.insert(stables.end(), t.begin(), t.end());
+      sp += N * p->dim;
+    }
+    p->total_stab = static_cast<uint32_t>(stables.size());
+  }
   QT_CUDA(cudaSetDevice(device));
   QT_CUDA(cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, device));
   QT_CUDA(cudaMalloc(&p->d_tables, p->host_tables.size()));
   QT_CUDA(cudaMemcpy(p->d_tables, p->host_tables.data(), p->host_tables.size(),
                      cudaMemcpyHostToDevice));
+  if (!stables.empty() && p->max_stab <= kMaxTableBytes) {
+    QT_CUDA(cudaMalloc(&p->d_stables, stables.size()));
+    QT_CUDA(cudaMemcpy(p->d_stables, stables.data(), stables.size(), cudaMemcpyHostToDevice));
+    QT_CUDA(cudaMalloc(&p->d_stab_off, n * sizeof(uint32_t)));
+    QT_CUDA(cudaMalloc(&p->d_stab_bytes, n * sizeof(uint32_t)));
+    QT_CUDA(cudaMemcpy(p->d_stab_off, soff.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    QT_CUDA(cudaMemcpy(p->d_stab_bytes, sbytes.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  }
   if (have_fast && p->max_ftab <= kMaxTableBytes) {
     QT_CUDA(cudaMalloc(&p->d_ftables, ftables.size()));
     QT_CUDA(cudaMemcpy(p->d_ftables, ftables.data(), ftables.size(), cudaMemcpyHostToDevice));
@@ -858,6 +946,27 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       p->fast_paths += count;
       g_launches.fetch_add(2);
       return 2;
+    }
+    if (p->d_stables && scan_enabled()) {  // d >= 2: FP32 scan + exact FP64 decision
+      // queries per thread: d = 2 keeps two CTAs per SM at P = 2; d = 3 is one
+      // CTA per SM anyway (64 KB tables), where P = 4 gives the ILP
+      int P = p->dim == 2 ? 2 : 4;
+      if (const char* e = std::getenv("QT_SCAN_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 2 ? 2 : 4;
+      const bool sres = p->total_stab <= kResidentBudget;
+      const uint32_t S = 3u * p->max_stab <= 200u * 1024u ? 3u : 2u;
+      const size_t ssmem = sres ? p->total_stab : static_cast<size_t>(S) * p->max_stab;
+      const int sbps = qt::paths_scan_blocks_per_sm(p->kind, src, sres, P, ssmem);
+      uint64_t sblocks = static_cast<uint64_t>(p->sm_count) * sbps;
+      const uint64_t per_block = 256ull * P;
+      const uint64_t sneed = (count + per_block - 1) / per_block;
+      if (sneed < sblocks) sblocks = sneed;
+      const uint64_t T = sblocks * per_block;
+      qt::ScanArgs sa{a, p->d_stables, p->d_stab_off, p->d_stab_bytes, p->max_stab, p->total_stab, S};
+      sa.p.q = count / T;
+      sa.p.rem = count % T;
+      QT_CUDA(qt::launch_paths_scan(p->kind, src, sres, P, sa, static_cast<uint32_t>(sblocks), ssmem, st));
+      g_launches.fetch_add(1);
+      return 1;
     }
     const int bps = qt::paths_blocks_per_sm(p->kind, src, resident, smem);
     uint64_t blocks = static_cast<uint64_t>(p->sm_count) * bps;

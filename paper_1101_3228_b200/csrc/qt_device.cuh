@@ -490,7 +490,7 @@ struct Chain<3> {  // GBM 3-D basket log-state
 // Exact scan over the sorted records (cold block, global memory) with
 // (d2, original index) ordering: identical result to the reference's
 // ascending strict-< scan for every x, including NaN / +-inf / overflow.
-__device__ __noinline__ uint32_t nearest_1d_scan(const Rec1* R, uint32_t n, double x) {
+static __device__ __noinline__ uint32_t nearest_1d_scan(const Rec1* R, uint32_t n, double x) {
   uint32_t best = 0;
   double bd = __longlong_as_double(0x7ff0000000000000ll);  // +inf
   for (uint32_t s = 0; s < n; ++s) {

@@ -63,6 +63,17 @@ struct FastArgs {
   uint32_t probe_nored;       // diagnostics only (QT_PROBE_NORED): skip the count REDs
 };
 
+// d >= 2 FP32-scan path kernel (qt_scan.cu)
+struct ScanArgs {
+  PathArgs p;                 // exact tables (p.tables: FP64 points, global) + joint + window
+  const uint8_t* stables;     // scan tables (ScanHdr + FP32 pairs), concatenated
+  const uint32_t* stab_off;   // [n]
+  const uint32_t* stab_bytes; // [n]
+  uint32_t sbuf_bytes;        // stage size (max scan table)
+  uint32_t sresident_bytes;   // sum of scan tables (resident mode)
+  uint32_t sstages;           // prefetch depth
+};
+
 struct Alg3Args {
   SrcArgs src;
   const uint8_t* tables;
@@ -94,6 +105,9 @@ cudaError_t launch_paths_fast(int kind, bool resident, int P, const FastArgs& a,
                               size_t smem, uint32_t replay_blocks, cudaStream_t st);
 int paths_fast_blocks_per_sm(int kind, bool resident, int P, size_t smem);
 cudaError_t launch_fast_bounds_check(unsigned int* out, cudaStream_t st);
+cudaError_t launch_paths_scan(int kind, int src, bool resident, int P, const ScanArgs& a,
+                              uint32_t blocks, size_t smem, cudaStream_t st);
+int paths_scan_blocks_per_sm(int kind, int src, bool resident, int P, size_t smem);
 cudaError_t launch_alg3(int kind, int src, const Alg3Args& a, uint32_t slices, size_t smem,
                         cudaStream_t st);
 cudaError_t launch_finalize(bool alg3, const unsigned long long* joint, unsigned long long* visits,

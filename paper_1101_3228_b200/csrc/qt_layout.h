@@ -119,6 +119,32 @@ inline uint32_t fbucket_host(double x, double gc, double bk_a, double bk_b, uint
   return b < nb1 ? b : nb1;
 }
 
+// ---------------------------------------------------------------------------
+// FP32 scan table (d >= 2; k_paths_scan). Points in ORIGINAL order, padded to
+// whole chunks of kScanChunkPairs pairs, stored as pairs of FP32 lanes so one
+// FFMA2 evaluates two points against a broadcast query coordinate:
+//   d == 2:  float4 XY[pair] = {x_a, x_b, y_a, y_b};  float2 H[pair] = {h_a, h_b}
+//   d == 3:  float4 XY[pair];                           float4 ZH[pair] = {z_a, z_b, h_a, h_b}
+// with h = fl32(|p|^2 / 2); the score s = h - q.p orders the points like
+// |q - p|^2 (= 2 s + |q|^2). Padding points have p = 0, h = +inf.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kScanChunkPairs = 16;  // 32 points per chunk
+
+struct alignas(16) ScanHdr {
+  double step[6];     // chain coefficients of transition k-1 -> k
+  uint64_t joff;      // element offset of joint[k-1]
+  uint64_t exact_off; // byte offset (from the exact tables base) of this layer's LayerTable
+  float hmax;         // max h over the layer
+  float pmax[3];      // max |p_c| per coordinate
+  uint32_t n_pts;     // N_k
+  uint32_t n_chunks;  // chunks of kScanChunkPairs pairs
+  uint32_t off_b;     // byte offset of H[] (d == 2) / ZH[] (d == 3)
+  uint32_t bytes;     // table bytes (multiple of 16)
+  uint32_t fp32_ok;   // all |p_c| < 2^40 (else every query takes the exact FP64 scan)
+  uint32_t pad_[7];
+};
+static_assert(sizeof(ScanHdr) == 128, "ScanHdr is 128 bytes");
+
 constexpr uint32_t kNoIndex = 0xFFFFFFFFu;
 
 // Bucket of x under a layer's (lo, inv_w, nb): identical IEEE operations on

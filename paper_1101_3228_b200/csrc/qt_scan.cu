@@ -1,0 +1,426 @@
+// qt_scan.cu -- K2 for d >= 2: the Voronoi projection as an FP32 brute-force
+// scan with an exact FP64 decision (TwoFactorChain d = 2, GbmChain3d d = 3).
+//
+// k_paths_scan runs Alg I / II paths like k_paths (exact FP64 normals and
+// chain step, estimate.hpp:88-126), but projects with
+//   pass 1  s_i = h_i - q . p_i for every grid point, two points per FFMA2
+//           (the query coordinate is the broadcast scalar operand), the
+//           per-chunk minimum by FMNMX3, and the three best chunk minima
+//           m1 <= m2 <= m3 per query (with the chunks of m1, m2);
+//   bound   |s_i - S_i| <= B(q) for the exact S_i = |p_i|^2/2 - q.p_i, and the
+//           reference's FP64 d2 (nn.hpp:25-45) orders like 2 S_i + |q|^2 up to
+//           a relative 2^-50, so every reference minimiser satisfies
+//           s_i <= tau = m1 + 2 B + 2^-48 (|m1| + B + |q|^2);
+//   pass 2  if the third-best chunk minimum m3 > tau, only the best (and,
+//           when m2 <= tau, the second-best) chunk of 32 points can hold a
+//           minimiser: the warp rescans each lane's chunk(s) cooperatively,
+//           one point per lane, and a ballot of s <= tau gives the
+//           candidates; one candidate is the answer, several are
+//           resolved with the reference's FP64 d2 in index order (strict <,
+//           smallest index on ties). Otherwise (or for a non-finite / huge
+//           query) the exact FP64 scan of nearest_2d / nearest_3d runs.
+// The cell is therefore always the reference's argmin; the FP32 scan only
+// decides which points need the FP64 arithmetic.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qt_device.cuh"
+#include "qt_internal.h"
+
+namespace qt {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanMaxStages = 4;
+
+// {s, s} * b + c on the FP32x2 pipe (SASS FFMA2 with a broadcast scalar)
+__device__ __forceinline__ float2 ffma2(float s, float2 b, float2 c) {
+  float2 r;
+  asm("{.reg .b64 a, b, c, d;\n\t"
+      "mov.b64 a, {%2, %2};\n\t"
+      "mov.b64 b, {%3, %4};\n\t"
+      "mov.b64 c, {%5, %6};\n\t"
+      "fma.rn.f32x2 d, a, b, c;\n\t"
+      "mov.b64 {%0, %1}, d;}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(s), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+
+// s of one pair of points against the query -q (negated, FP32)
+template <int D>
+__device__ __forceinline__ float2 pair_score(const float4* XY, const float4* B4, const float2* B2,
+                                             uint32_t pair, const float (&nq)[D]) {
+  const float4 xy = XY[pair];
+  float2 s;
+  if constexpr (D == 2) {
+    s = ffma2(nq[0], make_float2(xy.x, xy.y), B2[pair]);
+  } else {
+    const float4 zh = B4[pair];
+    s = ffma2(nq[2], make_float2(zh.x, zh.y), make_float2(zh.z, zh.w));
+    s = ffma2(nq[0], make_float2(xy.x, xy.y), s);
+  }
+  return ffma2(nq[1], make_float2(xy.z, xy.w), s);
+}
+
+// The reference's d2 of point idx (nn.hpp:25-45), FP64, from the exact table.
+template <int D>
+__device__ __forceinline__ double ref_d2(const LayerTable& hx, const uint8_t* xb, uint32_t idx,
+                                         const double (&q)[D]) {
+  const double* P = reinterpret_cast<const double*>(xb + hx.off_rec) + static_cast<uint64_t>(idx) * D;
+  if constexpr (D == 2) {
+    const double dx = __dsub_rn(q[0], P[0]);
+    const double dy = __dsub_rn(q[1], P[1]);
+    return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+  } else {
+    const double d0 = __dsub_rn(q[0], P[0]);
+    const double d1 = __dsub_rn(q[1], P[1]);
+    const double d2 = __dsub_rn(q[2], P[2]);
+    double acc = __dadd_rn(0.0, __dmul_rn(d0, d0));
+    acc = __dadd_rn(acc, __dmul_rn(d1, d1));
+    return __dadd_rn(acc, __dmul_rn(d2, d2));
+  }
+}
+
+// Projection of P queries against one staged scan table (see the file header).
+template <int D, int P>
+__device__ __forceinline__ void scan_project(const uint8_t* tb, const uint8_t* xtables,
+                                             const double (&x)[P][D], uint32_t (&cell)[P]) {
+  const ScanHdr& h = *reinterpret_cast<const ScanHdr*>(tb);
+  const float4* XY = reinterpret_cast<const float4*>(tb + sizeof(ScanHdr));
+  const float4* B4 = reinterpret_cast<const float4*>(tb + h.off_b);
+  const float2* B2 = reinterpret_cast<const float2*>(tb + h.off_b);
+  const uint32_t nch = h.n_chunks;
+  const float inf = __int_as_float(0x7f800000);
+  // best / second-best chunk minima and their chunks, third-best minimum
+  float nq[P][D], m1[P], m2[P], m3[P];
+  uint32_t b1[P], b2[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) nq[p][c] = -__double2float_rn(x[p][c]);
+    m1[p] = m2[p] = m3[p] = inf;
+    b1[p] = b2[p] = 0;
+  }
+  // pass 1: chunk minima, four pairs (eight points) per step reduced as a
+  // two-level FMNMX3 tree so the running minimum is not one long chain
+  for (uint32_t ch = 0; ch < nch; ++ch) {
+    float cm[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) cm[p] = inf;
+#pragma unroll 2
+    for (uint32_t j4 = 0; j4 < kScanChunkPairs; j4 += 4) {
+      float2 sv[P][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t pair = ch * kScanChunkPairs + j4 + u;
+        const float4 xy = XY[pair];
+        float2 hb;
+        float4 zh;
+        if constexpr (D == 2) hb = B2[pair];
+        else zh = B4[pair];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          float2 t;
+          if constexpr (D == 2) {
+            t = ffma2(nq[p][0], make_float2(xy.x, xy.y), hb);
+          } else {
+            t = ffma2(nq[p][2], make_float2(zh.x, zh.y), make_float2(zh.z, zh.w));
+            t = ffma2(nq[p][0], make_float2(xy.x, xy.y), t);
+          }
+          sv[p][u] = ffma2(nq[p][1], make_float2(xy.z, xy.w), t);
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < P; ++p) {  // FMNMX3 tree over 8 scores + the running min
+        const float a = fminf(fminf(sv[p][0].x, sv[p][0].y), sv[p][1].x);
+        const float b = fminf(fminf(sv[p][1].y, sv[p][2].x), sv[p][2].y);
+        const float c = fminf(fminf(sv[p][3].x, sv[p][3].y), cm[p]);
+        cm[p] = fminf(fminf(a, b), c);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const bool lt1 = cm[p] < m1[p], lt2 = cm[p] < m2[p];
+      m3[p] = fminf(m3[p], lt2 ? m2[p] : cm[p]);
+      m2[p] = lt1 ? m1[p] : (lt2 ? cm[p] : m2[p]);
+      b2[p] = lt1 ? b1[p] : (lt2 ? ch : b2[p]);
+      m1[p] = lt1 ? cm[p] : m1[p];
+      b1[p] = lt1 ? ch : b1[p];
+    }
+  }
+  const LayerTable& hx = *reinterpret_cast<const LayerTable*>(xtables + h.exact_off);
+  const uint8_t* xb = xtables + h.exact_off;
+  const uint32_t lane = threadIdx.x & 31u;
+  float tau[P];
+  bool ok[P], two[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    // B = 2^-24 1.01 (c_h hmax + c_q sum |q_c| pmax_c), all rounded up
+    float sq = 0.0f, qq = 0.0f, qmax = 0.0f;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const float av = fabsf(nq[p][c]);
+      sq = __fmaf_ru(av, h.pmax[c], sq);
+      qq = __fmaf_ru(av, av, qq);
+      qmax = fmaxf(qmax, av);
+    }
+    const float ch_ = D == 2 ? 3.1f : 4.1f, cq = D == 2 ? 4.1f : 5.1f;
+    const float B = __fmul_ru(0x1.02p-24f, __fmaf_ru(ch_, h.hmax, __fmul_ru(cq, sq)));
+    const float marg = __fmaf_ru(2.0f, B, __fmul_ru(0x1p-48f, __fadd_ru(__fadd_ru(fabsf(m1[p]), B), qq)));
+    tau[p] = __fadd_ru(m1[p], marg);
+    // candidates (s <= tau) lie in the best chunk, or also the second-best one
+    // when m2 <= tau, if the third-best chunk minimum m3 > tau
+    ok[p] = h.fp32_ok && qmax < 0x1p40f && m3[p] > tau[p];  // false for NaN too
+    two[p] = !(m2[p] > tau[p]);
+    if (two[p]) {  // candidate chunks in index order
+      const uint32_t lo = min(b1[p], b2[p]), hi = max(b1[p], b2[p]);
+      b1[p] = lo;
+      b2[p] = hi;
+    }
+  }
+  // pass 2, warp-cooperative: for every (lane l, query p) with ok, the warp
+  // rescans l's candidate chunk(s), one point per lane (the same FMA order as
+  // pass 1, so the same bits), and a ballot of s <= tau gives the candidates.
+  uint32_t cnt[P], first[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    cnt[p] = 0;
+    first[p] = 0;
+    unsigned pend = __ballot_sync(0xffffffffu, ok[p]);
+    while (pend) {
+      const uint32_t l = __ffs(pend) - 1;
+      pend &= pend - 1;
+      float q[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) q[c] = __shfl_sync(0xffffffffu, nq[p][c], l);
+      const float t = __shfl_sync(0xffffffffu, tau[p], l);
+      const uint32_t ca = __shfl_sync(0xffffffffu, b1[p], l);
+      const uint32_t cb = __shfl_sync(0xffffffffu, b2[p], l);
+      const bool tw = __shfl_sync(0xffffffffu, two[p] ? 1u : 0u, l) != 0u;
+      uint32_t c_cnt = 0, c_first = 0;
+      for (uint32_t w = 0; w < (tw ? 2u : 1u); ++w) {
+        const uint32_t cc = w ? cb : ca;
+        const uint32_t pair = cc * kScanChunkPairs + (lane >> 1);
+        const bool odd = lane & 1u;
+        const float4 xy = XY[pair];
+        const float X = odd ? xy.y : xy.x, Y = odd ? xy.w : xy.z;
+        float sv;
+        if constexpr (D == 2) {
+          const float2 hb = B2[pair];
+          sv = __fmaf_rn(q[0], X, odd ? hb.y : hb.x);
+        } else {
+          const float4 zh = B4[pair];
+          sv = __fmaf_rn(q[2], odd ? zh.y : zh.x, odd ? zh.w : zh.z);
+          sv = __fmaf_rn(q[0], X, sv);
+        }
+        sv = __fmaf_rn(q[1], Y, sv);
+        const unsigned m = __ballot_sync(0xffffffffu, sv <= t);
+        if (m && c_cnt == 0) c_first = cc * 2 * kScanChunkPairs + (__ffs(m) - 1);
+        c_cnt += __popc(m);
+      }
+      if (lane == l) {
+        cnt[p] = c_cnt;
+        first[p] = c_first;
+      }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    if (ok[p] && cnt[p] == 1) {
+      cell[p] = first[p];
+    } else if (ok[p]) {  // several candidates: the reference's d2 among them, in index order
+      uint32_t best = first[p];
+      double bd = ref_d2<D>(hx, xb, first[p], x[p]);
+      for (uint32_t w = 0; w < (two[p] ? 2u : 1u); ++w) {
+        const uint32_t cc = w ? b2[p] : b1[p];
+        for (uint32_t jj = 0; jj < kScanChunkPairs; ++jj) {
+          const uint32_t pair = cc * kScanChunkPairs + jj;
+          const float2 sc = pair_score<D>(XY, B4, B2, pair, nq[p]);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const uint32_t idx = 2 * pair + e;
+            if ((e ? sc.y : sc.x) <= tau[p] && idx > first[p]) {
+              const double d = ref_d2<D>(hx, xb, idx, x[p]);
+              if (d < bd) {
+                bd = d;
+                best = idx;
+              }
+            }
+          }
+        }
+      }
+      cell[p] = best;
+    } else {  // exact FP64 scan (nn.hpp:18-46)
+      cell[p] = nearest<D>(hx, xb, x[p], xtables);
+    }
+  }
+}
+
+template <int K, int SRC, bool RESIDENT, int P>
+__global__ void __launch_bounds__(kScanThreads, P >= 4 ? 1 : 2) k_paths_scan(const __grid_constant__ ScanArgs f) {
+  using C = Chain<K>;
+  constexpr int D = C::D;
+  const PathArgs& a = f.p;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[kScanMaxStages];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t S = f.sstages;
+  const uint64_t rounds = a.q + (a.rem ? 1u : 0u);
+  const uint64_t steps_total = rounds * a.n;
+  if (steps_total == 0) return;
+
+  auto issue = [&](uint64_t g) {
+    const uint32_t k = static_cast<uint32_t>(g % a.n);
+    const uint32_t st = static_cast<uint32_t>(g % S);
+    const uint32_t bytes = __ldg(f.stab_bytes + k);
+    mbar_expect_tx(&full[st], bytes);
+    bulk_g2s(smem + st * f.sbuf_bytes, f.stables + __ldg(f.stab_off + k), bytes, &full[st]);
+  };
+  if (tid == 0) {
+    for (uint32_t s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    if constexpr (RESIDENT) {
+      mbar_expect_tx(&full[0], f.sresident_bytes);
+      for (uint32_t k = 0; k < a.n; ++k)
+        bulk_g2s(smem + f.stab_off[k], f.stables + f.stab_off[k], f.stab_bytes[k], &full[0]);
+    } else {
+      for (uint64_t g = 0; g < S && g < steps_total; ++g) issue(g);
+    }
+  }
+  __syncthreads();
+
+  // P slots per thread, slot v = gid P + p owns a contiguous run of paths
+  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * kScanThreads + tid;
+  Source<SRC> src[P];
+  uint64_t beg[P], cnt[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const uint64_t v = gid * P + p;
+    cnt[p] = a.q + (v < a.rem ? 1u : 0u);
+    beg[p] = a.first + v * a.q + (v < a.rem ? v : a.rem);
+    if (cnt[p]) src[p].start(a.src, beg[p]);
+  }
+  if constexpr (RESIDENT) mbar_wait(&full[0], 0);
+  const uint32_t full0 = smem_u32(full);
+  uint32_t s = 0, ph = 0;
+  uint64_t g = 0;
+  const uint8_t* tb = smem;
+  for (uint64_t r = 0; r < rounds; ++r) {
+    double x[P][D];
+    uint32_t i[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (r < cnt[p] && r > 0) src[p].next_unit(a.src, beg[p] + r);
+#pragma unroll
+      for (int c = 0; c < D; ++c) x[p][c] = 0.0;  // initial(): the origin
+      i[p] = 0;
+    }
+    for (uint32_t k = 1; k <= a.n; ++k, ++g) {
+      if constexpr (RESIDENT) {
+        tb = smem + f.stab_off[k - 1];
+      } else {
+        mbar_wait_u32(full0 + 8u * s, ph);
+      }
+      const ScanHdr& h = *reinterpret_cast<const ScanHdr*>(tb);
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        if (r < cnt[p]) {
+          double e[C::NPS], xn[D];
+#pragma unroll
+          for (int q = 0; q < C::NPS; ++q) e[q] = src[p].normal();
+          C::step(h.step, x[p], xn, e);
+#pragma unroll
+          for (int c = 0; c < D; ++c) x[p][c] = xn[c];
+        }
+      }
+      uint32_t j[P];
+      scan_project<D, P>(tb, a.tables, x, j);
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        if (r < cnt[p]) {
+          red_add_u64(a.joint + h.joff + static_cast<uint64_t>(i[p]) * h.n_pts + j[p], 1ull);
+          i[p] = j[p];
+        }
+      }
+      if constexpr (!RESIDENT) {
+        named_barrier_sync(1, kScanThreads);  // every thread is done with stage s
+        if (tid == 0 && g + S < steps_total) issue(g + S);
+        tb += f.sbuf_bytes;
+        if (++s == S) {
+          s = 0;
+          ph ^= 1u;
+          tb = smem;
+        }
+      }
+    }
+  }
+}
+
+template <int K, int SRC, bool RES, int P>
+static cudaError_t launch_scan_t(const ScanArgs& a, uint32_t blocks, size_t smem, cudaStream_t st) {
+  auto fn = k_paths_scan<K, SRC, RES, P>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  fn<<<blocks, kScanThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int K, int SRC, bool RES, int P>
+static int scan_bps_t(size_t smem) {
+  auto fn = k_paths_scan<K, SRC, RES, P>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kScanThreads, smem) != cudaSuccess)
+    return 1;
+  return nb > 0 ? nb : 1;
+}
+
+template <int K, int SRC>
+static cudaError_t scan_dispatch_p(bool query, int* bps, bool res, int P, const ScanArgs& a,
+                                   uint32_t blocks, size_t smem, cudaStream_t st) {
+#define QT_SCAN_CASE(PP)                                                                    \
+  if (P == PP) {                                                                            \
+    if (query) {                                                                            \
+      *bps = res ? scan_bps_t<K, SRC, true, PP>(smem) : scan_bps_t<K, SRC, false, PP>(smem); \
+      return cudaSuccess;                                                                   \
+    }                                                                                       \
+    return res ? launch_scan_t<K, SRC, true, PP>(a, blocks, smem, st)                       \
+               : launch_scan_t<K, SRC, false, PP>(a, blocks, smem, st);                     \
+  }
+  QT_SCAN_CASE(1)
+  QT_SCAN_CASE(4)
+  QT_SCAN_CASE(2)
+#undef QT_SCAN_CASE
+  return cudaErrorInvalidValue;
+}
+
+template <int K>
+static cudaError_t scan_dispatch_s(bool query, int* bps, int src, bool res, int P,
+                                   const ScanArgs& a, uint32_t blocks, size_t smem,
+                                   cudaStream_t st) {
+  switch (src) {
+    case kSrcLcg48: return scan_dispatch_p<K, kSrcLcg48>(query, bps, res, P, a, blocks, smem, st);
+    case kSrcMrg: return scan_dispatch_p<K, kSrcMrg>(query, bps, res, P, a, blocks, smem, st);
+    case kSrcXorwow: return scan_dispatch_p<K, kSrcXorwow>(query, bps, res, P, a, blocks, smem, st);
+    default: return scan_dispatch_p<K, kSrcNormalsIn>(query, bps, res, P, a, blocks, smem, st);
+  }
+}
+
+// k_paths_scan for kind 1 (TwoFactorChain, d = 2) / 3 (GbmChain3d, d = 3)
+cudaError_t launch_paths_scan(int kind, int src, bool resident, int P, const ScanArgs& a,
+                              uint32_t blocks, size_t smem, cudaStream_t st) {
+  int dummy = 0;
+  return kind == 1 ? scan_dispatch_s<1>(false, &dummy, src, resident, P, a, blocks, smem, st)
+                   : scan_dispatch_s<3>(false, &dummy, src, resident, P, a, blocks, smem, st);
+}
+
+int paths_scan_blocks_per_sm(int kind, int src, bool resident, int P, size_t smem) {
+  int bps = 1;
+  ScanArgs dummy{};
+  if (kind == 1) scan_dispatch_s<1>(true, &bps, src, resident, P, dummy, 0, smem, nullptr);
+  else scan_dispatch_s<3>(true, &bps, src, resident, P, dummy, 0, smem, nullptr);
+  return bps;
+}
+
+}  // namespace qt

@@ -1,0 +1,111 @@
+"""K2 for d >= 2: the FP32 brute-force scan with an exact FP64 decision
+(k_paths_scan, qt_scan.cu) must give exactly the reference's cells.
+
+Checked against the exact FP64 kernel (QT_SCAN=0 selects it) on the config-4
+and config-5 chains and grids, on adversarial grids (exact ties, near-ties
+closer than the FP32 error bound, coordinates too large for FP32, far-away
+queries), and against the CPU oracle on windows of the config chains."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from pyoracle import CHAIN_GBM3D, CHAIN_TWO_FACTOR, ChainSpec
+
+pytestmark = pytest.mark.gpu
+
+
+def Q():
+    from paper_1101_3228_b200 import qtree
+    return qtree
+
+
+def _counts(monkeypatch, chain, grids, M, first=0, total=None, scan=True, engine=1):
+    import torch
+    from paper_1101_3228_b200.device import Plan
+    monkeypatch.setenv("QT_SCAN", "1" if scan else "0")
+    plan = Plan(chain, grids, 0)
+    joint = plan.zeros_joint()
+    plan.count(1, engine, 12345, first, M, total or M, joint)
+    torch.cuda.synchronize()
+    plan.close()
+    return joint.cpu().numpy().view(np.uint64).copy()
+
+
+def test_scan_equals_exact_c4(gpu, monkeypatch):
+    q = Q()
+    tf = q.TwoFactorChain(q.TwoFactorParams())
+    g4 = q.build_two_factor_grids(tf, 1000)
+    for first in (0, 31415926):
+        a = _counts(monkeypatch, tf, g4, 20000, first, 10**8, True)
+        b = _counts(monkeypatch, tf, g4, 20000, first, 10**8, False)
+        assert np.array_equal(a, b), first
+        assert int(a[:1000].sum()) == 20000
+
+
+def test_scan_equals_exact_c5(gpu, monkeypatch):
+    q = Q()
+    ch = q.GbmChain3d(20, 1.0, (0.0, 0.0, 0.0))
+    g5 = q.build_gbm_grids(ch, 4000)
+    a = _counts(monkeypatch, ch, g5, 20000, 777, 4 * 10**9, True)
+    b = _counts(monkeypatch, ch, g5, 20000, 777, 4 * 10**9, False)
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("engine", [0, 2])
+def test_scan_other_engines(gpu, monkeypatch, engine):
+    q = Q()
+    tf = q.TwoFactorChain(q.TwoFactorParams(steps=30))
+    g = q.build_two_factor_grids(tf, 1000)
+    assert np.array_equal(_counts(monkeypatch, tf, g, 30000, 0, None, True, engine),
+                          _counts(monkeypatch, tf, g, 30000, 0, None, False, engine))
+
+
+@pytest.mark.parametrize("case", ["ties", "near_ties", "huge", "far", "tiny_grid"])
+def test_scan_adversarial_grids(gpu, monkeypatch, case):
+    q = Q()
+    n = 8
+    tf = q.TwoFactorChain(q.TwoFactorParams(steps=n))
+    rng = np.random.default_rng(3)
+    grids = []
+    for k in range(1, n + 1):
+        if case == "ties":  # lattice: many exactly equidistant pairs -> smallest index
+            xs = np.linspace(-1, 1, 9)
+            pts = np.array([(a, b) for a in xs for b in xs]).reshape(-1)
+        elif case == "near_ties":  # pairs mirrored to ~1e-9: below the FP32 bound
+            base = rng.standard_normal((150, 2)) * 0.5
+            pts = np.concatenate([base, -base + 1e-9]).reshape(-1)
+        elif case == "huge":  # FP32 cannot hold these: every query takes the FP64 scan
+            pts = rng.standard_normal(400) * 1e13
+        elif case == "far":  # queries far outside a small cluster
+            pts = rng.standard_normal(400) * 1e-3 + 5.0
+        else:  # fewer points than one chunk
+            pts = rng.standard_normal(6)
+        grids.append(q.QuantGrid(2, pts))
+    a = _counts(monkeypatch, tf, grids, 50000, 0, None, True)
+    b = _counts(monkeypatch, tf, grids, 50000, 0, None, False)
+    assert np.array_equal(a, b), case
+
+
+def test_scan_c4_window_vs_oracle(gpu, oracle):
+    q = Q()
+    tf = q.TwoFactorChain(q.TwoFactorParams())
+    g4 = q.build_two_factor_grids(tf, 1000)
+    spec4 = ChainSpec(CHAIN_TWO_FACTOR, 365)
+    s4 = np.array([1] + [1000] * 365, np.uint64)
+    p4 = np.concatenate([g.data() for g in g4])
+    v, j = q.accumulate_paths(tf, g4, 1, 12345, 98765, 1000, 10**8)
+    rv, rj = oracle.accumulate_paths(spec4, s4, p4, 1, 12345, 98765, 1000, 10**8)
+    assert np.array_equal(v, rv) and np.array_equal(j, rj)
+
+
+def test_scan_c5_window_vs_oracle(gpu, oracle):
+    q = Q()
+    ch = q.GbmChain3d(20, 1.0, (0.0, 0.0, 0.0))
+    g5 = q.build_gbm_grids(ch, 4000)
+    spec5 = ChainSpec(CHAIN_GBM3D, 20, gbm_rho=(0.0, 0.0, 0.0))
+    s5 = np.array([1] + [4000] * 20, np.uint64)
+    p5 = np.concatenate([g.data() for g in g5])
+    v, j = q.accumulate_paths(ch, g5, 1, 12345, 2 * 10**9, 800, 4 * 10**9)
+    rv, rj = oracle.accumulate_paths(spec5, s5, p5, 1, 12345, 2 * 10**9, 800, 4 * 10**9)
+    assert np.array_equal(v, rv) and np.array_equal(j, rj)
