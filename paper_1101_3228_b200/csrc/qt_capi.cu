@@ -39,6 +39,12 @@ std::atomic<int> g_fast{-1};
 // cumulative fast-path evidence of destroyed plans: paths, replayed, inline-replayed
 std::atomic<uint64_t> g_fast_paths{0}, g_fast_replayed{0}, g_fast_inline{0};
 
+// 1-D MRG32k3a lockstep exact kernel: enabled unless QT_XKERNEL=0 (then k_paths)
+bool xkernel_enabled() {
+  const char* e = std::getenv("QT_XKERNEL");
+  return !(e && e[0] == '0');
+}
+
 // d >= 2 FP32-scan kernel: enabled unless QT_SCAN=0
 bool scan_enabled() {
   const char* e = std::getenv("QT_SCAN");
@@ -946,6 +952,27 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       p->fast_paths += count;
       g_launches.fetch_add(2);
       return 2;
+    }
+    if (src == QT_ENGINE_MRG32K3A && (p->kind == QT_CHAIN_BROWNIAN_1D || p->kind == QT_CHAIN_OU_1D) &&
+        xkernel_enabled()) {  // 1-D MRG32k3a: the lockstep exact kernel
+      int P = 2;
+      if (const char* e = std::getenv("QT_X_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 4 ? 4 : 2;
+      qt::PathArgs xa = a;
+      xa.stages = 3u * p->max_tab <= 150u * 1024u ? 3u : 2u;
+      const size_t xsmem = resident ? p->total_tab : static_cast<size_t>(xa.stages) * p->max_tab;
+      int xbps = 1;
+      QT_CUDA(qt::launch_paths_x(p->kind, resident, P, xa, 0, xsmem, st, &xbps));
+      uint64_t xblocks = static_cast<uint64_t>(p->sm_count) * xbps;
+      const uint64_t per_block = 256ull * P;
+      const uint64_t xneed = (count + per_block - 1) / per_block;
+      if (xneed < xblocks) xblocks = xneed;
+      const uint64_t T = xblocks * per_block;
+      xa.q = count / T;
+      xa.rem = count % T;
+      QT_CUDA(qt::launch_paths_x(p->kind, resident, P, xa, static_cast<uint32_t>(xblocks), xsmem, st,
+                                 nullptr));
+      g_launches.fetch_add(1);
+      return 1;
     }
     if (p->d_stables && scan_enabled()) {  // d >= 2: FP32 scan + exact FP64 decision
       // queries per thread: d = 2 keeps two CTAs per SM at P = 2; d = 3 is one

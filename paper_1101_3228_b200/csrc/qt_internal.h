@@ -105,6 +105,8 @@ cudaError_t launch_paths_fast(int kind, bool resident, int P, const FastArgs& a,
                               size_t smem, uint32_t replay_blocks, cudaStream_t st);
 int paths_fast_blocks_per_sm(int kind, bool resident, int P, size_t smem);
 cudaError_t launch_fast_bounds_check(unsigned int* out, cudaStream_t st);
+cudaError_t launch_paths_x(int kind, bool resident, int P, const PathArgs& a, uint32_t blocks,
+                           size_t smem, cudaStream_t st, int* bps);
 cudaError_t launch_paths_scan(int kind, int src, bool resident, int P, const ScanArgs& a,
                               uint32_t blocks, size_t smem, cudaStream_t st);
 int paths_scan_blocks_per_sm(int kind, int src, bool resident, int P, size_t smem);

@@ -380,6 +380,193 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_fast(const __grid_consta
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_paths_x: the exact 1-D path kernel for MRG32k3a (Brownian / OU), i.e.
+// k_paths' arithmetic bit for bit, in the lockstep CTA pipeline of
+// k_paths_fast: no producer warp, one named barrier per layer, thread 0
+// prefetching the next S - 1 layer tables, P paths in flight per thread so
+// one table wait and one header read serve P transitions, and the Box-Muller
+// pair drawn with two interleaved MRG32k3a steps.
+// ---------------------------------------------------------------------------
+struct ExactPath {
+  Mrg st;
+  double x;     // state (chains.hpp: origin at the path start)
+  double zs;    // Box-Muller mate
+  uint32_t i;   // cell at the previous layer
+};
+
+template <int K, int P>
+__device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act)[P],
+                                            const uint8_t* tb, uint32_t k,
+                                            unsigned long long* joint, const uint8_t* gtables) {
+  using C = Chain<K>;
+  const LayerTable& h = *reinterpret_cast<const LayerTable*>(tb);
+  const double x_safe = h.x_safe, lo = h.lo, inv_w = h.inv_w, nb_d = h.nb_d;
+  const uint32_t nb = h.nb, npts = h.n_pts;
+  const Thr* T = reinterpret_cast<const Thr*>(tb + h.off_rec);
+  const uint16_t* start = reinterpret_cast<const uint16_t*>(tb + h.off_start);
+  unsigned long long* jl = joint + h.joff;
+  double z[P];
+  if (k & 1u) {  // a fresh pair (stream.hpp:97-108): z1 now, z2 cached
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      uint32_t u1, u2;
+      mrg_step2(ps[p].st, u1, u2);
+      box_muller(mrg_to_unit(u1), mrg_to_unit(u2), z[p], ps[p].zs);
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < P; ++p) z[p] = ps[p].zs;
+  }
+  uint32_t c[P];
+  bool safe[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    double xn[1], e[1] = {z[p]}, xo[1] = {ps[p].x};
+    C::step(h.step, xo, xn, e);
+    ps[p].x = xn[0];
+    safe[p] = fabs(xn[0]) < x_safe;
+    c[p] = start[bucket_of(safe[p] ? xn[0] : 0.0, lo, inv_w, nb_d, nb)];  // all t_{<c} < x
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const double x = ps[p].x;
+    uint32_t j;
+    if (safe[p]) {
+      const Thr r0 = T[c[p]], r1 = T[c[p] + 1];
+      if (x < r0.t) {
+        j = r0.orig;
+      } else if (x < r1.t) {
+        j = r1.orig;
+      } else {
+        uint32_t cc = c[p] + 2;
+        while (!(x < T[cc].t)) ++cc;  // t_{N-1} = +inf stops the walk
+        j = T[cc].orig;
+      }
+    } else {  // exact scan over the cold block (NaN / inf / |x| >= x_safe)
+      j = nearest_1d_scan(reinterpret_cast<const Rec1*>(gtables + h.cold_off), npts, x);
+    }
+    if (act[p]) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + j, 1ull);
+    ps[p].i = j;
+  }
+}
+
+template <int K, bool RESIDENT, int P>
+__global__ void __launch_bounds__(kFastThreads) k_paths_x(const __grid_constant__ PathArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[kMaxStages];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t S = a.stages;
+  const uint64_t rounds = a.q + (a.rem ? 1u : 0u);
+  const uint64_t steps_total = rounds * a.n;
+  if (steps_total == 0) return;
+  auto issue = [&](uint64_t g) {
+    const uint32_t k = static_cast<uint32_t>(g % a.n);
+    const uint32_t st = static_cast<uint32_t>(g % S);
+    const uint32_t bytes = __ldg(a.tab_bytes + k);
+    mbar_expect_tx(&full[st], bytes);
+    bulk_g2s(smem + st * a.buf_bytes, a.tables + __ldg(a.tab_off + k), bytes, &full[st]);
+  };
+  if (tid == 0) {
+    for (uint32_t s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    if constexpr (RESIDENT) {
+      mbar_expect_tx(&full[0], a.resident_bytes);
+      for (uint32_t k = 0; k < a.n; ++k)
+        bulk_g2s(smem + (a.tab_off[k] - a.tab_off[0]), a.tables + a.tab_off[k], a.tab_bytes[k],
+                 &full[0]);
+    } else {
+      for (uint64_t g = 0; g < S && g < steps_total; ++g) issue(g);
+    }
+  }
+  __syncthreads();
+
+  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * kFastThreads + tid;
+  ExactPath ps[P];
+  uint64_t cnt[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const uint64_t v = gid * P + p;
+    cnt[p] = a.q + (v < a.rem ? 1u : 0u);
+    const uint64_t beg = a.first + v * a.q + (v < a.rem ? v : a.rem);
+    ps[p].st = Mrg{};
+    if (cnt[p]) {
+      Source<kSrcMrg> src;
+      src.start(a.src, beg);
+      ps[p].st = src.s;
+    }
+  }
+  if constexpr (RESIDENT) mbar_wait(&full[0], 0);
+  const uint32_t full0 = smem_u32(full);
+  uint32_t s = 0, ph = 0;
+  uint64_t g = 0;
+  const uint8_t* tb = smem;
+  for (uint64_t r = 0; r < rounds; ++r) {
+    bool act[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      act[p] = r < cnt[p];
+      ps[p].x = 0.0;  // chains.hpp:43-46,81: the origin
+      ps[p].i = 0;    // layer 0 is the singleton {x0}
+    }
+    for (uint32_t k = 1; k <= a.n; ++k, ++g) {
+      if constexpr (RESIDENT) {
+        tb = smem + (a.tab_off[k - 1] - a.tab_off[0]);
+      } else {
+        mbar_wait_u32(full0 + 8u * s, ph);
+      }
+      exact_layer<K, P>(ps, act, tb, k, a.joint, a.tables);
+      if constexpr (!RESIDENT) {
+        named_barrier_sync(1, kFastThreads);  // every thread is done with stage s
+        if (tid == 0 && g + S < steps_total) issue(g + S);
+        tb += a.buf_bytes;
+        if (++s == S) {
+          s = 0;
+          ph ^= 1u;
+          tb = smem;
+        }
+      }
+    }
+  }
+}
+
+template <int K, bool RES, int P>
+static cudaError_t launch_x_t(const PathArgs& a, uint32_t blocks, size_t smem, cudaStream_t st,
+                              int* bps) {
+  auto fn = k_paths_x<K, RES, P>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  if (bps) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, fn, kFastThreads, smem) != cudaSuccess ||
+        *bps < 1)
+      *bps = 1;
+    return cudaSuccess;
+  }
+  fn<<<blocks, kFastThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int K>
+static cudaError_t launch_x_k(bool res, int P, const PathArgs& a, uint32_t blocks, size_t smem,
+                              cudaStream_t st, int* bps) {
+  if (P == 1)
+    return res ? launch_x_t<K, true, 1>(a, blocks, smem, st, bps)
+               : launch_x_t<K, false, 1>(a, blocks, smem, st, bps);
+  if (P == 4)
+    return res ? launch_x_t<K, true, 4>(a, blocks, smem, st, bps)
+               : launch_x_t<K, false, 4>(a, blocks, smem, st, bps);
+  return res ? launch_x_t<K, true, 2>(a, blocks, smem, st, bps)
+             : launch_x_t<K, false, 2>(a, blocks, smem, st, bps);
+}
+
+// k_paths_x (kind 0 = Brownian, 2 = OU; MRG32k3a). bps != nullptr: occupancy query only.
+cudaError_t launch_paths_x(int kind, bool resident, int P, const PathArgs& a, uint32_t blocks,
+                           size_t smem, cudaStream_t st, int* bps) {
+  return kind == 0 ? launch_x_k<0>(resident, P, a, blocks, smem, st, bps)
+                   : launch_x_k<2>(resident, P, a, blocks, smem, st, bps);
+}
+
 // The replay list of one k_paths_fast launch, grid-stride.
 template <int K>
 __global__ void __launch_bounds__(256) k_replay(const __grid_constant__ FastArgs f) {
