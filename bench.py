@@ -370,6 +370,11 @@ def run_ours(args, rank, world, local_rank):
     # algorithmic bytes of the path kernel: 16 B per transition (one u64 RMW)
     kern_units = count * n if est != 2 else count
     achieved = 16.0 * kern_units / (t_kern / 1e3) / 1e9
+    kernel_name = {"bm": "k_paths_x (exact 1-D path kernel: MRG32k3a + FP64 Box-Muller + step + "
+                         "threshold projection + RED count)",
+                   "ou": "k_alg3 (layer-parallel pair sampler)" if est == 2 else "k_paths_x",
+                   "tf": "k_paths_scan (FP64 path + FP32 FFMA2 brute-force scan, exact decision)",
+                   "gbm": "k_paths_scan (FP64 path + FP32 FFMA2 brute-force scan, exact decision)"}[kind]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
@@ -384,9 +389,10 @@ def run_ours(args, rank, world, local_rank):
                      "traffic": profiled_traffic(args.config, kern_units),
                      "traffic_unit": "GB per launch (ncu dram read+write)",
                      "algorithmic_gb_per_launch": 16.0 * kern_units / 1e9,
-                     "kernel": "k_paths (fused RNG + step + projection + count)",
+                     "kernel": kernel_name,
                      "kernel_ms": t_kern, "peak_source": peak_src,
-                     "algorithmic_bytes": "16 B per transition (u64 counter read-modify-write)"},
+                     "algorithmic_bytes": "16 B per transition (u64 counter read-modify-write)",
+                     "binding_unit": "L2 atomic (RED) throughput + issue, see DESIGN.md section 4"},
         "e2e": {"value": transitions / (t_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e, "steps": e2e_steps},
         "gpu_launches": int(my_launches),
@@ -397,6 +403,15 @@ def run_ours(args, rank, world, local_rank):
     if price is not None:
         crr = crr_bermudan_put(100.0, 100.0, 0.05, 0.2, 1.0, n)
         line["price"] = {"put": price, "crr_bermudan": crr, "rel_err_vs_crr": abs(price - crr) / crr}
+    if kind in ("tf", "gbm"):  # FP32-bound configs: 3 d N flop per transition
+        fp32_peak = 72.24  # profiles/r01_peaks_fp.json (FFMA microbenchmark, this pool)
+        flops = 3.0 * (2 if kind == "tf" else 3) * N * kern_units
+        line["roofline_fp32"] = {"bound": "fp32", "achieved": flops / (t_kern / 1e3) / 1e12,
+                                 "peak": fp32_peak, "unit": "TFLOP/s",
+                                 "frac": flops / (t_kern / 1e3) / 1e12 / fp32_peak,
+                                 "algorithmic_flops": "3 d N per transition (brute-force "
+                                                      "convention, PAPER.md:540-543)",
+                                 "peak_source": "profiles/r01_peaks_fp.json"}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, args.ref_seconds)
     print(json.dumps(line), flush=True)
