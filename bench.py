@@ -345,6 +345,11 @@ def run_ours(args, rank, world, local_rank):
     d2h = (plan.n_visits + 2 * plan.n_joint) * 8
     h2d = int(sum(g.data().nbytes for g in grids) + plan.sizes.nbytes + ch.step_coef.nbytes +
               ch.marg_coef.nbytes)
+    # one untimed call: process-level one-time costs (pinned staging buffers, module load)
+    if world == 1:
+        Q.estimate(est, ch, grids, min(M, 10**6))
+    else:
+        estimate_distributed(est, ch, grids, min(M, 10**6))
     for _ in range(e2e_steps):
         torch.cuda.synchronize()
         barrier()

@@ -19,6 +19,7 @@
 #include <limits>
 #include <mutex>
 #include <numeric>
+#include <thread>
 #include <string>
 #include <memory>
 #include <vector>
@@ -652,7 +653,8 @@ TableBlob build_table(int kind, int dim, uint64_t npts, const double* pts, const
       while (c + 1 < npts && qt::bucket_of(t[c], lo, inv_w, h.nb_d, nb) < b) ++c;
       start[b] = static_cast<uint16_t>(std::min<uint64_t>(c, 65535));
     }
-    if ((kind == QT_CHAIN_BROWNIAN_1D || kind == QT_CHAIN_OU_1D) && npts <= 65535)
+    if ((kind == QT_CHAIN_BROWNIAN_1D || kind == QT_CHAIN_OU_1D) && npts <= 65535 &&
+        fast_enabled())
       out.fast = build_fast_table(kind, t, ord, x_safe, step, joff);
     out.cold.assign(16ull * npts, 0);
     Rec1* R = reinterpret_cast<Rec1*>(out.cold.data());
@@ -1085,6 +1087,56 @@ double ms_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// Device -> pageable host copy through a pinned double buffer: the DMA of chunk
+// c+1 overlaps the (multi-threaded) memcpy of chunk c into the caller's buffer.
+// A plain cudaMemcpy into pageable memory runs at a few GB/s (staging + page
+// faults on freshly allocated output arrays); this keeps PCIe/C2C busy.
+void d2h_pinned(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  constexpr size_t kChunk = 32u << 20;
+  static std::mutex mu;
+  static uint8_t* pin[2] = {nullptr, nullptr};
+  std::lock_guard<std::mutex> lk(mu);
+  if (bytes < (4u << 20)) {  // small: direct
+    QT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    QT_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  if (!pin[0]) {
+    QT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&pin[0]), kChunk, cudaHostAllocDefault));
+    QT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&pin[1]), kChunk, cudaHostAllocDefault));
+  }
+  cudaEvent_t ev[2];
+  QT_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  QT_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  auto par_copy = [](uint8_t* d, const uint8_t* s, size_t n) {
+    constexpr int kT = 4;
+    std::vector<std::thread> th;
+    const size_t per = (n + kT - 1) / kT;
+    for (int t = 1; t < kT; ++t) {
+      const size_t b = per * t, e = std::min(n, b + per);
+      if (b < e) th.emplace_back([=] { std::memcpy(d + b, s + b, e - b); });
+    }
+    std::memcpy(d, s, std::min(n, per));
+    for (auto& x : th) x.join();
+  };
+  const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+  auto issue = [&](size_t c) {
+    const size_t off = c * kChunk, n = std::min(kChunk, bytes - off);
+    QT_CUDA(cudaMemcpyAsync(pin[c & 1], static_cast<const uint8_t*>(src) + off, n,
+                            cudaMemcpyDeviceToHost, st));
+    QT_CUDA(cudaEventRecord(ev[c & 1], st));
+  };
+  issue(0);
+  for (size_t c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) issue(c + 1);
+    QT_CUDA(cudaEventSynchronize(ev[c & 1]));
+    const size_t off = c * kChunk, n = std::min(kChunk, bytes - off);
+    par_copy(static_cast<uint8_t*>(dst) + off, pin[c & 1], n);
+  }
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+}
+
 // Shared body of qt_estimate / qt_estimate_normals / qt_accumulate_paths.
 void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_t samples,
                   int engine, uint64_t seed, int devices, const double* h_normals,
@@ -1129,9 +1181,14 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
     cudaFree(d_vis);
     cudaFree(d_pi);
   };
+  const bool dbg = std::getenv("QT_DEBUG") != nullptr;
+  auto mark = [&](const char* what) {
+    if (dbg) std::fprintf(stderr, "qtree: %-12s %9.2f ms\n", what, ms_since(t0));
+  };
   try {
     for (int g = 0; g < G; ++g) {
       plans[g].reset(make_plan(chain, grids, g));
+      mark("plan");
       QT_CUDA(cudaSetDevice(g));
       QT_CUDA(cudaStreamCreateWithFlags(&streams[g], cudaStreamNonBlocking));
       for (int e = 0; e < 4; ++e) QT_CUDA(cudaEventCreate(&ev[4 * g + e]));
@@ -1146,6 +1203,7 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
       QT_CUDA(cudaMemcpyAsync(d_normals, h_normals, count * per * sizeof(double),
                               cudaMemcpyHostToDevice, streams[0]));
     }
+    mark("alloc");
     // shard g: units [first + count g / G, first + count (g+1) / G)  (estimate.hpp:180-181)
     for (int g = 0; g < G; ++g) {
       const uint64_t b = first + static_cast<uint64_t>(static_cast<u128>(count) * g / G);
@@ -1194,12 +1252,12 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
       QT_CUDA(cudaMemcpyAsync(hv.data(), d_vis, p0->nvis * 8, cudaMemcpyDeviceToHost, streams[0]));
       QT_CUDA(cudaMemcpyAsync(hj.data(), dj[0], p0->njoint * 8, cudaMemcpyDeviceToHost, streams[0]));
     } else {
-      QT_CUDA(cudaMemcpyAsync(visits, d_vis, p0->nvis * 8, cudaMemcpyDeviceToHost, streams[0]));
-      QT_CUDA(cudaMemcpyAsync(joint, dj[0], p0->njoint * 8, cudaMemcpyDeviceToHost, streams[0]));
-      if (pi)
-        QT_CUDA(cudaMemcpyAsync(pi, d_pi, p0->njoint * 8, cudaMemcpyDeviceToHost, streams[0]));
+      d2h_pinned(visits, d_vis, p0->nvis * 8, streams[0]);
+      d2h_pinned(joint, dj[0], p0->njoint * 8, streams[0]);
+      if (pi) d2h_pinned(pi, d_pi, p0->njoint * 8, streams[0]);
     }
     QT_CUDA(cudaStreamSynchronize(streams[0]));
+    mark("d2h done");
     if (accumulate) {
       for (uint64_t i = 0; i < p0->nvis; ++i) visits[i] += hv[i];
       for (uint64_t i = 0; i < p0->njoint; ++i) joint[i] += hj[i];

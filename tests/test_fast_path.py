@@ -28,6 +28,15 @@ def Q():
     return qtree
 
 
+@pytest.fixture(autouse=True)
+def fast_on():
+    """The fast path is opt-in: its tables are built by plans created while it
+    is enabled; each test leaves it disabled again."""
+    Q().set_fast_path(True)
+    yield
+    Q().set_fast_path(False)
+
+
 def _counts(plan, M, first=0, total=None, fast=True):
     import torch
     q = Q()
@@ -125,7 +134,6 @@ def test_fast_window_vs_oracle(gpu, oracle):
     sizes = np.array([1] + [500] * 50, np.uint64)
     pts = np.concatenate([g.data() for g in grids])
     first = 314159265
-    q.set_fast_path(True)
     v, j = q.accumulate_paths(ch, grids, 1, 12345, first, 40000, 10**9)
     rv, rj = oracle.accumulate_paths(spec, sizes, pts, 1, 12345, first, 40000, 10**9)
     assert np.array_equal(v, rv) and np.array_equal(j, rj)
