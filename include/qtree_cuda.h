@@ -175,6 +175,26 @@ QT_API qt_status qt_bdp_swing(int32_t layers, const uint64_t* sizes, const uint6
 QT_API qt_status qt_bdp_cond_expectation(uint64_t rows, uint64_t cols, const uint64_t* row_visits,
                                          const double* pi, const double* f, double* out);
 
+/* ---- tree and grid files (quant_tree.hpp:138-207, grid.hpp:84-117) ---------
+ * Byte-identical to the reference's save_tree / save_grid; loaders raise the
+ * reference's IoError (status 3) messages, NumericError (4) for grid
+ * invariants. points_all holds layers 0..n (layer 0 = {x0}), the other arrays
+ * are laid out as in qt_estimate. device_arrays != 0: visits / joint / pi are
+ * DEVICE pointers, streamed to the file through pinned staging buffers (no
+ * host copy of the tree). */
+QT_API qt_status qt_save_tree(const char* path, int32_t layers, int32_t dim, const uint64_t* sizes,
+                              const double* points_all, uint64_t samples, const uint64_t* visits,
+                              const uint64_t* joint, const double* pi, int32_t device_arrays);
+/* Header of a tree file: n, dim, M and (nullable) sizes[0..n], to size the arrays. */
+QT_API qt_status qt_tree_file_info(const char* path, int32_t* layers, int32_t* dim,
+                                   uint64_t* samples, uint64_t* sizes);
+QT_API qt_status qt_load_tree(const char* path, uint64_t* sizes, double* points_all,
+                              uint64_t* visits, uint64_t* joint, double* pi);
+QT_API qt_status qt_save_grid(const char* path, int32_t dim, uint64_t n, const double* pts);
+/* *dim, *n always; pts (nullable) is filled when cap (doubles) >= n * dim. */
+QT_API qt_status qt_load_grid(const char* path, int32_t* dim, uint64_t* n, double* pts,
+                              uint64_t cap);
+
 /* ---- diagnostics ----------------------------------------------------------- */
 
 /* The exact normals the in-kernel engine feeds path m in [first, first+count)

@@ -101,6 +101,15 @@ OQ_EXPORT int oq_solve_swing(int n, const uint64_t* sizes, const uint64_t* visit
                              const double* pi, const double* phi, int qmin, int qmax,
                              double* price, double* value_all);
 
+/* Tree / grid files through the reference's own save_tree / load_tree /
+ * save_grid (reference harness only; the restatement does not export them). */
+OQ_EXPORT int oq_save_tree(const char* path, int n, int dim, const uint64_t* sizes,
+                           const double* pts_all, uint64_t samples, const uint64_t* visits,
+                           const uint64_t* joint, const double* pi);
+OQ_EXPORT int oq_load_tree(const char* path, int* n, int* dim, uint64_t* samples, uint64_t* sizes,
+                           double* pts_all, uint64_t* visits, uint64_t* joint, double* pi);
+OQ_EXPORT int oq_save_grid(const char* path, int dim, uint64_t npts, const double* pts);
+
 #ifdef __cplusplus
 }
 #endif

@@ -249,6 +249,46 @@ class Oracle:
                                             _p(out, C.c_double)), "build_grids")
         return out
 
+    # --- files (reference harness only: the reference's own save_tree etc.) ---
+    def save_tree(self, path, dim, sizes, pts_all, samples, visits, joint, pi):
+        sizes = np.ascontiguousarray(sizes, dtype=np.uint64)
+        L = self.lib
+        L.oq_save_tree.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_uint64),
+                                   C.POINTER(C.c_double), C.c_uint64, C.POINTER(C.c_uint64),
+                                   C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        pa = np.ascontiguousarray(pts_all, dtype=np.float64)
+        v = np.ascontiguousarray(visits, dtype=np.uint64)
+        j = np.ascontiguousarray(joint, dtype=np.uint64)
+        pi_ = np.ascontiguousarray(pi, dtype=np.float64)
+        self._check(L.oq_save_tree(str(path).encode(), len(sizes) - 1, dim, _p(sizes, C.c_uint64),
+                                   _p(pa, C.c_double), samples, _p(v, C.c_uint64),
+                                   _p(j, C.c_uint64), _p(pi_, C.c_double)), "save_tree")
+
+    def load_tree(self, path, max_layers, max_points, max_joint):
+        L = self.lib
+        u64p, f64p, ip = C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_int)
+        L.oq_load_tree.argtypes = [C.c_char_p, ip, ip, u64p, u64p, f64p, u64p, u64p, f64p]
+        n, d, m = C.c_int(0), C.c_int(0), C.c_uint64(0)
+        sizes = np.zeros(max_layers + 1, np.uint64)
+        pts = np.zeros(max_points, np.float64)
+        v = np.zeros(max_points, np.uint64)
+        j = np.zeros(max_joint, np.uint64)
+        pi = np.zeros(max_joint, np.float64)
+        self._check(L.oq_load_tree(str(path).encode(), C.byref(n), C.byref(d), C.byref(m),
+                                   _p(sizes, C.c_uint64), _p(pts, C.c_double), _p(v, C.c_uint64),
+                                   _p(j, C.c_uint64), _p(pi, C.c_double)), "load_tree")
+        sizes = sizes[:n.value + 1]
+        nvis, njoint = layout(sizes)
+        return (n.value, d.value, m.value, sizes, pts[:nvis * d.value], v[:nvis], j[:njoint],
+                pi[:njoint])
+
+    def save_grid(self, path, dim, pts):
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        L = self.lib
+        L.oq_save_grid.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.POINTER(C.c_double)]
+        self._check(L.oq_save_grid(str(path).encode(), dim, pts.size // dim, _p(pts, C.c_double)),
+                    "save_grid")
+
     def lloyd_base(self, dim, grid_size, seed=12345, per_iter=0, iterations=40):
         out = np.zeros(grid_size * dim, np.float64)
         self._check(self.lib.oq_lloyd_base(dim, grid_size, seed, per_iter, iterations,

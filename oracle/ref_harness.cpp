@@ -517,4 +517,64 @@ int oq_solve_swing(int n, const uint64_t* sizes, const uint64_t* visits, const d
   });
 }
 
+// tree::save_tree / load_tree (quant_tree.hpp:138-207) and quant::save_grid /
+// load_grid (grid.hpp:84-117), the reference's own writers and readers.
+int oq_save_tree(const char* path, int n, int dim, const uint64_t* sizes, const double* pts_all,
+                 uint64_t samples, const uint64_t* visits, const uint64_t* joint,
+                 const double* pi) {
+  return guarded([&] {
+    tree::QuantTree t;
+    t.samples = samples;
+    t.counts.visits.resize(static_cast<std::size_t>(n) + 1);
+    t.counts.joint.resize(static_cast<std::size_t>(n));
+    t.pi.resize(static_cast<std::size_t>(n));
+    std::size_t vo = 0, jo = 0, go = 0;
+    for (int k = 0; k <= n; ++k) {
+      const std::size_t N = sizes[k];
+      t.grids.emplace_back(dim, std::vector<double>(pts_all + go, pts_all + go + N * dim));
+      go += N * dim;
+      t.counts.visits[static_cast<std::size_t>(k)].assign(visits + vo, visits + vo + N);
+      vo += N;
+    }
+    for (int k = 1; k <= n; ++k) {
+      const std::size_t len = static_cast<std::size_t>(sizes[k - 1] * sizes[k]);
+      t.counts.joint[static_cast<std::size_t>(k - 1)].assign(joint + jo, joint + jo + len);
+      t.pi[static_cast<std::size_t>(k - 1)].assign(pi + jo, pi + jo + len);
+      jo += len;
+    }
+    tree::save_tree(t, path);
+  });
+}
+
+int oq_load_tree(const char* path, int* n, int* dim, uint64_t* samples, uint64_t* sizes,
+                 double* pts_all, uint64_t* visits, uint64_t* joint, double* pi) {
+  return guarded([&] {
+    const tree::QuantTree t = tree::load_tree(path);
+    *n = t.layers();
+    *dim = t.grids[0].dim();
+    *samples = t.samples;
+    std::size_t vo = 0, jo = 0, go = 0;
+    for (int k = 0; k <= *n; ++k) {
+      const auto& g = t.grids[static_cast<std::size_t>(k)];
+      sizes[k] = g.size();
+      for (double v : g.data()) pts_all[go++] = v;
+      for (auto v : t.counts.visits[static_cast<std::size_t>(k)]) visits[vo++] = v;
+    }
+    for (int k = 1; k <= *n; ++k) {
+      const auto& J = t.counts.joint[static_cast<std::size_t>(k - 1)];
+      const auto& P = t.pi[static_cast<std::size_t>(k - 1)];
+      for (std::size_t e = 0; e < J.size(); ++e, ++jo) {
+        joint[jo] = J[e];
+        pi[jo] = P[e];
+      }
+    }
+  });
+}
+
+int oq_save_grid(const char* path, int dim, uint64_t npts, const double* pts) {
+  return guarded([&] {
+    quant::save_grid(quant::QuantGrid(dim, std::vector<double>(pts, pts + npts * dim)), path);
+  });
+}
+
 }  // extern "C"

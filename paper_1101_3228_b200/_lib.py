@@ -61,6 +61,13 @@ _SIGS = {
     "qt_fast_stats": [_u64p],
     "qt_plan_fast_stats": [C.c_void_p, _u64p],
     "qt_fast_bounds_check": [_f64p],
+    "qt_save_tree": [C.c_char_p, C.c_int32, C.c_int32, _u64p, _f64p, C.c_uint64, C.c_void_p,
+                     C.c_void_p, C.c_void_p, C.c_int32],
+    "qt_tree_file_info": [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                          C.POINTER(C.c_uint64), _u64p],
+    "qt_load_tree": [C.c_char_p, _u64p, _f64p, _u64p, _u64p, _f64p],
+    "qt_save_grid": [C.c_char_p, C.c_int32, C.c_uint64, _f64p],
+    "qt_load_grid": [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_uint64), _f64p, C.c_uint64],
 }
 
 # Every symbol include/qtree_cuda.h declares (checked by tests/test_boundary.py).

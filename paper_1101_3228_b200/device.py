@@ -69,6 +69,22 @@ class Plan:
         return n.value
 
 
+    def save_tree(self, path, samples: int, joint: torch.Tensor, visits: torch.Tensor,
+                  pi: torch.Tensor, x0=None) -> None:
+        """Write the device-resident tree as QTRE v1 (quant_tree.hpp:138-163) straight
+        from HBM through pinned staging buffers (no host copy of the counts / pi)."""
+        import numpy as np
+        torch.cuda.synchronize(self.device)
+        dim = self.chain.dim()
+        x0 = np.zeros(dim) if x0 is None else np.asarray(x0, np.float64)
+        pts = np.ascontiguousarray(np.concatenate([x0, self._gp.points]), np.float64)
+        sizes = np.ascontiguousarray(self.sizes, np.uint64)
+        _check(L.lib().qt_save_tree(str(path).encode(), len(sizes) - 1, dim,
+                                    sizes.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                    pts.ctypes.data_as(C.POINTER(C.c_double)), int(samples),
+                                    C.c_void_p(visits.data_ptr()), C.c_void_p(joint.data_ptr()),
+                                    C.c_void_p(pi.data_ptr()), 1), "save_tree")
+
     def fast_stats(self) -> dict:
         """Fast 1-D path evidence of this plan (synchronises its device)."""
         out = (C.c_uint64 * 3)()

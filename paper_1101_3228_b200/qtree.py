@@ -389,6 +389,57 @@ def path_normals(engine, seed, normals_per_path, first, count) -> np.ndarray:
     return out
 
 
+# ---------------------------------------------------------------------------
+# files (quant_tree.hpp:138-207 save_tree / load_tree, grid.hpp:84-117)
+# ---------------------------------------------------------------------------
+def save_tree(tree: QuantTree, path) -> None:
+    """QTRE v1, byte-identical to the reference's save_tree."""
+    dim = tree.grids[0].dim()
+    pts = np.ascontiguousarray(np.concatenate([np.asarray(g.data(), np.float64) for g in tree.grids]))
+    sizes = np.ascontiguousarray(tree.sizes, np.uint64)
+    v = np.ascontiguousarray(tree.flat_visits, np.uint64)
+    j = np.ascontiguousarray(tree.flat_joint, np.uint64)
+    p = np.ascontiguousarray(tree.flat_pi, np.float64)
+    _check(L.lib().qt_save_tree(str(path).encode(), tree.layers(), dim, _u(sizes), _f(pts),
+                                tree.samples, v.ctypes.data, j.ctypes.data, p.ctypes.data, 0),
+           "save_tree")
+
+
+def load_tree(path) -> QuantTree:
+    n, d, m = C.c_int32(0), C.c_int32(0), C.c_uint64(0)
+    _check(L.lib().qt_tree_file_info(str(path).encode(), C.byref(n), C.byref(d), C.byref(m),
+                                     None), "load_tree")
+    sizes = np.zeros(n.value + 1, np.uint64)
+    _check(L.lib().qt_tree_file_info(str(path).encode(), C.byref(n), C.byref(d), C.byref(m),
+                                     _u(sizes)), "load_tree")
+    nvis, njoint = layout(sizes)
+    pts = np.zeros(nvis * d.value, np.float64)
+    v = np.zeros(nvis, np.uint64)
+    j = np.zeros(njoint, np.uint64)
+    p = np.zeros(njoint, np.float64)
+    _check(L.lib().qt_load_tree(str(path).encode(), _u(sizes), _f(pts), _u(v), _u(j), _f(p)),
+           "load_tree")
+    grids, o = [], 0
+    for s in sizes:
+        grids.append(QuantGrid(d.value, pts[o:o + int(s) * d.value]))
+        o += int(s) * d.value
+    return QuantTree(grids, sizes, v, j, p, m.value)
+
+
+def save_grid(grid: QuantGrid, path) -> None:
+    pts = np.ascontiguousarray(grid.data(), np.float64)
+    _check(L.lib().qt_save_grid(str(path).encode(), grid.dim(), grid.size(), _f(pts)), "save_grid")
+
+
+def load_grid(path) -> QuantGrid:
+    d, n = C.c_int32(0), C.c_uint64(0)
+    _check(L.lib().qt_load_grid(str(path).encode(), C.byref(d), C.byref(n), None, 0), "load_grid")
+    pts = np.zeros(n.value * d.value, np.float64)
+    _check(L.lib().qt_load_grid(str(path).encode(), C.byref(d), C.byref(n), _f(pts), pts.size),
+           "load_grid")
+    return QuantGrid(d.value, pts)
+
+
 def set_fast_path(enabled: bool) -> None:
     """Select the fast 1-D path (FP32 Box-Muller + certified cells + exact
     replay; identical counts) or the exact FP64 kernel for every path."""
