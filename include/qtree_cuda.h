@@ -175,6 +175,19 @@ QT_API qt_status qt_bdp_swing(int32_t layers, const uint64_t* sizes, const uint6
 QT_API qt_status qt_bdp_cond_expectation(uint64_t rows, uint64_t cols, const uint64_t* row_visits,
                                          const double* pi, const double* f, double* out);
 
+/* ---- grid construction (lloyd.hpp:59-107, pipeline.hpp:27-77) -------------
+ * lloyd_build with the standard-normal sampler on the serial MRG32k3a stream
+ * seeded `stream_seed` (the reference's grid builders pass seed ^ 0x9E3779B9):
+ * distinct initial centers in stream order, then `iterations` batches of
+ * samples_per_iter samples, exact projection, recentering of non-empty cells
+ * in the reference's summation order. normals (nullable) replaces the stream
+ * (parity mode: bit-identical grids). distortion (nullable): per-iteration
+ * mean squared distance under the old centers. */
+QT_API qt_status qt_lloyd_build(int32_t dim, uint64_t n_points, int32_t iterations,
+                                uint64_t samples_per_iter, uint64_t stream_seed,
+                                const double* normals, uint64_t n_normals, double* centers,
+                                double* distortion);
+
 /* ---- tree and grid files (quant_tree.hpp:138-207, grid.hpp:84-117) ---------
  * Byte-identical to the reference's save_tree / save_grid; loaders raise the
  * reference's IoError (status 3) messages, NumericError (4) for grid

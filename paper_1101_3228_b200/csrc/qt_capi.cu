@@ -19,6 +19,7 @@
 #include <limits>
 #include <mutex>
 #include <numeric>
+#include <set>
 #include <thread>
 #include <string>
 #include <memory>
@@ -1390,6 +1391,134 @@ QT_API qt_status qt_plan_finalize(qt_plan* plan, int32_t estimator, uint64_t sam
     const int l = plan_finalize(plan, estimator, samples, d_joint, d_visits, d_pi,
                                 static_cast<cudaStream_t>(stream));
     if (launches) *launches = l;
+  });
+}
+
+// lloyd_build (lloyd.hpp:59-107) with the GaussianSampler on the serial
+// MRG32k3a stream seeded `stream_seed` (the pipeline passes seed ^ 0x9E3779B9,
+// pipeline.hpp:35,63). normals (nullable): the stream's normals supplied by the
+// caller (parity mode), at least as many as the build consumes.
+QT_API qt_status qt_lloyd_build(int32_t dim, uint64_t n_points, int32_t iterations,
+                                uint64_t samples_per_iter, uint64_t stream_seed,
+                                const double* normals, uint64_t n_normals, double* centers,
+                                double* distortion) {
+  return guarded([&] {
+    if (n_points == 0) raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: need at least one center");
+    if (iterations < 0) raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: iterations must be >= 0");
+    if (dim < 1 || dim > 3) raise(QT_ERR_NUMERIC, "lloyd_build: sampler dimension mismatch");
+    if (!centers) raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: null output");
+    if (samples_per_iter == 0 && iterations > 0)
+      raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: samples_per_iter must be >= 1");
+    if (samples_per_iter > 0x7fffffffull || n_points > 0x7fffffffull)
+      raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: batch too large");
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+      raise(QT_ERR_DEVICE, "cuda: no CUDA device available (the build has no CPU path)");
+    QT_CUDA(cudaSetDevice(0));
+    const uint64_t d = static_cast<uint64_t>(dim), N = n_points, M = samples_per_iter;
+    const qt::SrcArgs src = make_src(0, QT_ENGINE_MRG32K3A, stream_seed, 1, 1, nullptr, 0);
+    cudaStream_t st = nullptr;
+    std::vector<void*> bufs;
+    auto dalloc = [&](size_t bytes) {
+      void* p = nullptr;
+      QT_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+      bufs.push_back(p);
+      return p;
+    };
+    auto cleanup = [&] {
+      for (void* p : bufs) cudaFree(p);
+      if (st) cudaStreamDestroy(st);
+    };
+    try {
+      QT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      uint64_t consumed = 0;  // normals of the stream used so far
+      auto fetch = [&](double* dst_dev, uint64_t count) {
+        if (normals) {
+          if (consumed + count > n_normals)
+            raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: not enough normals supplied");
+          QT_CUDA(cudaMemcpyAsync(dst_dev, normals + consumed, count * 8, cudaMemcpyHostToDevice, st));
+        } else {
+          QT_CUDA(qt::launch_serial_normals(src, consumed, count, dst_dev, st));
+          g_launches.fetch_add(1);
+        }
+        consumed += count;
+      };
+      // initial centers: distinct samples in stream order (lloyd.hpp:72-83)
+      std::vector<double> c;
+      c.reserve(N * d);
+      {
+        std::set<std::vector<double>> seen;
+        uint64_t attempts = 0;
+        const uint64_t batch = (N + 64) * d;
+        double* dn = static_cast<double*>(dalloc(batch * 8));
+        std::vector<double> h(batch);
+        while (c.size() < N * d) {
+          fetch(dn, batch);
+          QT_CUDA(cudaMemcpyAsync(h.data(), dn, batch * 8, cudaMemcpyDeviceToHost, st));
+          QT_CUDA(cudaStreamSynchronize(st));
+          uint64_t used = 0;
+          for (; used + d <= batch && c.size() < N * d; used += d) {
+            std::vector<double> x(h.begin() + used, h.begin() + used + d);
+            if (seen.insert(x).second) c.insert(c.end(), x.begin(), x.end());
+            if (++attempts > 100 * N + 100)
+              raise(QT_ERR_NUMERIC, "lloyd_build: sampler cannot produce enough distinct centers");
+          }
+          consumed -= batch - used;  // hand the unused normals back to the stream
+        }
+      }
+      if (iterations > 0) {
+        double* dX = static_cast<double*>(dalloc(M * d * 8));
+        double* dC = static_cast<double*>(dalloc(N * d * 8));
+        double* dd2 = static_cast<double*>(dalloc(M * 8));
+        auto* dcell = static_cast<unsigned long long*>(dalloc(M * 8));
+        auto* key = static_cast<uint32_t*>(dalloc(M * 4));
+        auto* idx = static_cast<uint32_t*>(dalloc(M * 4));
+        auto* key2 = static_cast<uint32_t*>(dalloc(M * 4));
+        auto* idx2 = static_cast<uint32_t*>(dalloc(M * 4));
+        auto* cnt = static_cast<uint32_t*>(dalloc(N * 4));
+        auto* offs = static_cast<uint32_t*>(dalloc(N * 4));
+        const size_t tmp_bytes = qt::lloyd_tmp_bytes(M, N);
+        void* tmp = dalloc(tmp_bytes);
+        uint8_t* dT = nullptr;
+        size_t dT_bytes = 0;
+        std::vector<double> hd2(M);
+        QT_CUDA(cudaMemcpyAsync(dC, c.data(), N * d * 8, cudaMemcpyHostToDevice, st));
+        for (int it = 0; it < iterations; ++it) {
+          // snapshot grid (lloyd.hpp:88-89): the reference's QuantGrid checks
+          check_grid(dim, N, c.data(), 0);
+          double zeros[6] = {0, 0, 0, 0, 0, 0};
+          TableBlob tb = build_table(-1, dim, N, c.data(), zeros, zeros, 0, 1, 1);
+          std::vector<uint8_t> t = tb.hot;
+          const uint32_t hot_bytes = static_cast<uint32_t>(t.size());
+          set_cold_off(t, t.size());
+          t.insert(t.end(), tb.cold.begin(), tb.cold.end());
+          if (t.size() > dT_bytes) {
+            dT = static_cast<uint8_t*>(dalloc(t.size()));
+            dT_bytes = t.size();
+          }
+          QT_CUDA(cudaMemcpyAsync(dT, t.data(), t.size(), cudaMemcpyHostToDevice, st));
+          fetch(dX, M * d);
+          QT_CUDA(qt::launch_nearest(dim, dT, hot_bytes, dX, M, dcell, st));
+          QT_CUDA(qt::launch_lloyd_update(dX, dcell, M, N, dim, dC, dd2, key, idx, key2, idx2, cnt,
+                                          offs, tmp, tmp_bytes, st));
+          g_launches.fetch_add(4);
+          QT_CUDA(cudaMemcpyAsync(hd2.data(), dd2, M * 8, cudaMemcpyDeviceToHost, st));
+          QT_CUDA(cudaMemcpyAsync(c.data(), dC, N * d * 8, cudaMemcpyDeviceToHost, st));
+          QT_CUDA(cudaStreamSynchronize(st));
+          if (distortion) {  // dist_sum in sample order (lloyd.hpp:94-97)
+            double sum = 0.0;
+            for (uint64_t m = 0; m < M; ++m) sum += hd2[m];
+            distortion[it] = sum / static_cast<double>(M);
+          }
+        }
+      }
+      check_grid(dim, N, c.data(), 0);  // result.grid = QuantGrid(dim, centers)
+      std::memcpy(centers, c.data(), N * d * 8);
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
   });
 }
 

@@ -105,6 +105,13 @@ cudaError_t launch_paths_fast(int kind, bool resident, int P, const FastArgs& a,
                               size_t smem, uint32_t replay_blocks, cudaStream_t st);
 int paths_fast_blocks_per_sm(int kind, bool resident, int P, size_t smem);
 cudaError_t launch_fast_bounds_check(unsigned int* out, cudaStream_t st);
+cudaError_t launch_serial_normals(const SrcArgs& a, uint64_t first, uint64_t count, double* out,
+                                  cudaStream_t st);
+cudaError_t launch_lloyd_update(const double* X, const unsigned long long* cell, uint64_t M,
+                                uint64_t N, int d, double* centers, double* d2, uint32_t* key,
+                                uint32_t* idx, uint32_t* key2, uint32_t* idx2, uint32_t* counts,
+                                uint32_t* offs, void* tmp, size_t tmp_bytes, cudaStream_t st);
+size_t lloyd_tmp_bytes(uint64_t M, uint64_t N);
 cudaError_t launch_paths_x(int kind, bool resident, int P, const PathArgs& a, uint32_t blocks,
                            size_t smem, cudaStream_t st, int* bps);
 cudaError_t launch_paths_scan(int kind, int src, bool resident, int P, const ScanArgs& a,

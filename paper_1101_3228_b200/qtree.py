@@ -582,13 +582,40 @@ def cond_expectation(tree: QuantTree, k: int, f) -> np.ndarray:
 _DATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "base_grids.npz")
 
 
+@dataclass
+class LloydResult:
+    grid: "QuantGrid"
+    distortion: np.ndarray
+
+
+def lloyd_build(dim: int, n_points: int, iterations: int = 40, samples_per_iter: int = 0,
+                seed: int = 12345, normals=None) -> LloydResult:
+    """Randomized Lloyd on the GPU (lloyd.hpp:59-107) with the standard-normal
+    sampler, on the serial MRG32k3a stream the reference's grid builders use
+    (seed ^ 0x9E3779B9, pipeline.hpp:35,63). samples_per_iter 0 -> max(20000,
+    200 N) (pipeline.hpp:18-20). normals: the stream's normals supplied (parity
+    mode, bit-identical to the reference)."""
+    spi = samples_per_iter or max(20000, 200 * n_points)
+    out = np.zeros(n_points * dim, np.float64)
+    dist = np.zeros(max(iterations, 1), np.float64)
+    nrm = None if normals is None else np.ascontiguousarray(normals, np.float64)
+    _check(L.lib().qt_lloyd_build(int(dim), int(n_points), int(iterations), int(spi),
+                                  (int(seed) ^ 0x9E3779B9) & 0xFFFFFFFFFFFFFFFF,
+                                  None if nrm is None else _f(nrm),
+                                  0 if nrm is None else nrm.size, _f(out), _f(dist)),
+           "lloyd_build")
+    return LloydResult(QuantGrid(dim, out), dist[:iterations])
+
+
 def base_grid(grid_size: int, dim: int) -> np.ndarray:
+    """The standard-normal base quantizer of the grid builders: the reference's
+    own lloyd_build output where shipped (bit-identical, data/base_grids.npz),
+    else built on the GPU by lloyd_build (normals <= 1 ulp from glibc)."""
     key = f"n{grid_size}_d{dim}"
     with np.load(_DATA) as z:
-        if key not in z:
-            raise ValueError(f"no base quantizer {key} in {_DATA} (grid construction is out of "
-                             "scope for the device path; see DESIGN.md)")
-        return np.array(z[key])
+        if key in z:
+            return np.array(z[key])
+    return np.asarray(lloyd_build(dim, grid_size).grid.data(), np.float64)
 
 
 def _cholesky2_marginal(p: TwoFactorParams, t: float):
