@@ -188,6 +188,18 @@ QT_API qt_status qt_lloyd_build(int32_t dim, uint64_t n_points, int32_t iteratio
                                 const double* normals, uint64_t n_normals, double* centers,
                                 double* distortion);
 
+/* ---- micro-benchmarks (qtree_main.cpp bench-rng / bench-nn) -------------- */
+/* estimate_pi_partitioned (monte_carlo.hpp:51-77): samples uniforms (a positive
+ * multiple of 2*streams) in `streams` block (skip_ahead = 0) or skip-ahead
+ * streams; the integer inside-count equals the reference's. ms = device time. */
+QT_API qt_status qt_bench_pi(int32_t engine, uint64_t seed, uint64_t samples, uint64_t streams,
+                             int32_t skip_ahead, uint64_t* inside, double* estimate,
+                             double* std_error, double* ms);
+/* bench-nn: n 2-D grid points then `queries` queries from one MRG32k3a stream;
+ * sink = sum of nearest indices, ms = device time of the searches. */
+QT_API qt_status qt_bench_nn(uint64_t n, uint64_t queries, uint64_t seed, uint64_t* sink,
+                             double* ms);
+
 /* ---- tree and grid files (quant_tree.hpp:138-207, grid.hpp:84-117) ---------
  * Byte-identical to the reference's save_tree / save_grid; loaders raise the
  * reference's IoError (status 3) messages, NumericError (4) for grid

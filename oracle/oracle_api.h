@@ -109,6 +109,10 @@ OQ_EXPORT int oq_save_tree(const char* path, int n, int dim, const uint64_t* siz
 OQ_EXPORT int oq_load_tree(const char* path, int* n, int* dim, uint64_t* samples, uint64_t* sizes,
                            double* pts_all, uint64_t* visits, uint64_t* joint, double* pi);
 OQ_EXPORT int oq_save_grid(const char* path, int dim, uint64_t npts, const double* pts);
+/* bench-rng / bench-nn through the reference code (reference harness only). */
+OQ_EXPORT int oq_bench_pi(int engine, uint64_t seed, uint64_t samples, uint64_t streams, int skip,
+                          double* estimate, double* std_error);
+OQ_EXPORT int oq_bench_nn(uint64_t n, uint64_t queries, uint64_t seed, uint64_t* sink);
 
 #ifdef __cplusplus
 }

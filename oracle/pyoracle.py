@@ -289,6 +289,22 @@ class Oracle:
         self._check(L.oq_save_grid(str(path).encode(), dim, pts.size // dim, _p(pts, C.c_double)),
                     "save_grid")
 
+    def bench_pi(self, engine, seed, samples, streams, skip):
+        L = self.lib
+        L.oq_bench_pi.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                  C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        e, se = C.c_double(0), C.c_double(0)
+        self._check(L.oq_bench_pi(engine, seed, samples, streams, int(skip), C.byref(e),
+                                  C.byref(se)), "bench_pi")
+        return e.value, se.value
+
+    def bench_nn(self, n, queries, seed):
+        L = self.lib
+        L.oq_bench_nn.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]
+        s = C.c_uint64(0)
+        self._check(L.oq_bench_nn(n, queries, seed, C.byref(s)), "bench_nn")
+        return s.value
+
     def lloyd_base(self, dim, grid_size, seed=12345, per_iter=0, iterations=40):
         out = np.zeros(grid_size * dim, np.float64)
         self._check(self.lib.oq_lloyd_base(dim, grid_size, seed, per_iter, iterations,

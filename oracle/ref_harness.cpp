@@ -26,6 +26,7 @@
 #include "qtree/quant/lloyd.hpp"
 #include "qtree/quant/nn.hpp"
 #include "qtree/rng/stream.hpp"
+#include "qtree/rng/monte_carlo.hpp"
 #include "qtree/tree/estimate.hpp"
 
 #include "oracle_api.h"
@@ -574,6 +575,34 @@ int oq_load_tree(const char* path, int* n, int* dim, uint64_t* samples, uint64_t
 int oq_save_grid(const char* path, int dim, uint64_t npts, const double* pts) {
   return guarded([&] {
     quant::save_grid(quant::QuantGrid(dim, std::vector<double>(pts, pts + npts * dim)), path);
+  });
+}
+
+// bench-rng / bench-nn bodies (qtree_main.cpp:136-191) on the reference code
+int oq_bench_pi(int engine, uint64_t seed, uint64_t samples, uint64_t streams, int skip,
+                double* estimate, double* std_error) {
+  return guarded([&] {
+    const auto est = rng::estimate_pi_partitioned(
+        engine_of(engine), seed, samples, streams,
+        skip ? rng::PartitionMode::SkipAhead : rng::PartitionMode::Block);
+    *estimate = est.estimate;
+    *std_error = est.std_error;
+  });
+}
+
+int oq_bench_nn(uint64_t n, uint64_t queries, uint64_t seed, uint64_t* sink) {
+  return guarded([&] {
+    rng::RngStream g = rng::split_stream(rng::EngineKind::Mrg32k3a, seed, rng::StreamPartition{});
+    std::vector<double> pts(2 * n);
+    for (auto& v : pts) v = g.next_gaussian();
+    const quant::QuantGrid grid(2, std::move(pts));
+    const quant::NnIndex index(grid, quant::NnBackend::BruteForce);
+    std::vector<double> qs(2 * queries);
+    for (auto& v : qs) v = g.next_gaussian();
+    std::size_t s = 0;
+    for (std::uint64_t q = 0; q < queries; ++q)
+      s += index.nearest(std::span<const double>(qs.data() + 2 * q, 2));
+    *sink = s;
   });
 }
 

@@ -63,6 +63,9 @@ _SIGS = {
     "qt_fast_bounds_check": [_f64p],
     "qt_lloyd_build": [C.c_int32, C.c_uint64, C.c_int32, C.c_uint64, C.c_uint64, _f64p, C.c_uint64,
                        _f64p, _f64p],
+    "qt_bench_pi": [C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, _u64p, _f64p,
+                    _f64p, _f64p],
+    "qt_bench_nn": [C.c_uint64, C.c_uint64, C.c_uint64, _u64p, _f64p],
     "qt_save_tree": [C.c_char_p, C.c_int32, C.c_int32, _u64p, _f64p, C.c_uint64, C.c_void_p,
                      C.c_void_p, C.c_void_p, C.c_int32],
     "qt_tree_file_info": [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),

@@ -1522,6 +1522,119 @@ QT_API qt_status qt_lloyd_build(int32_t dim, uint64_t n_points, int32_t iteratio
   });
 }
 
+// estimate_pi_partitioned (monte_carlo.hpp:51-77) on the GPU
+QT_API qt_status qt_bench_pi(int32_t engine, uint64_t seed, uint64_t samples, uint64_t streams,
+                             int32_t skip_ahead, uint64_t* inside, double* estimate,
+                             double* std_error, double* ms) {
+  return guarded([&] {
+    if (engine < 0 || engine > 2) raise(QT_ERR_CONFIG, "bench-rng: unknown engine");
+    if (streams == 0) raise(QT_ERR_INVALID_ARGUMENT, "estimate_pi_partitioned: streams must be >= 1");
+    if (samples == 0 || samples % (2 * streams) != 0)
+      raise(QT_ERR_INVALID_ARGUMENT,
+            "estimate_pi_partitioned: sample count must be a positive multiple of 2*streams");
+    if (engine == QT_ENGINE_XORWOW && skip_ahead && streams > 1)
+      raise(QT_ERR_INVALID_ARGUMENT, "split_stream: skip-ahead is unsupported for xorwow");
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+      raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
+    QT_CUDA(cudaSetDevice(0));
+    const qt::SrcArgs a = make_src(0, engine, seed, 1, 1, nullptr, 0);
+    unsigned long long* d = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    auto fin = [&] {
+      cudaFree(d);
+      if (e0) cudaEventDestroy(e0);
+      if (e1) cudaEventDestroy(e1);
+    };
+    try {
+      QT_CUDA(cudaMalloc(&d, 8));
+      QT_CUDA(cudaMemset(d, 0, 8));
+      QT_CUDA(cudaEventCreate(&e0));
+      QT_CUDA(cudaEventCreate(&e1));
+      QT_CUDA(cudaEventRecord(e0));
+      QT_CUDA(qt::launch_pi(engine, skip_ahead, a, samples, streams, d, nullptr));
+      QT_CUDA(cudaEventRecord(e1));
+      g_launches.fetch_add(1);
+      unsigned long long in = 0;
+      QT_CUDA(cudaMemcpy(&in, d, 8, cudaMemcpyDeviceToHost));
+      float t = 0;
+      QT_CUDA(cudaEventElapsedTime(&t, e0, e1));
+      const uint64_t points = samples / 2;  // pi_from_counts (monte_carlo.hpp:31-35)
+      const double est = 4.0 * static_cast<double>(in) / static_cast<double>(points);
+      if (inside) *inside = in;
+      if (estimate) *estimate = est;
+      if (std_error) *std_error = std::sqrt(est * (4.0 - est) / static_cast<double>(points));
+      if (ms) *ms = t;
+    } catch (...) {
+      fin();
+      throw;
+    }
+    fin();
+  });
+}
+
+// `qtree bench-nn` (qtree_main.cpp:162-191): a 2-D grid of n standard-normal
+// points and `queries` standard-normal queries from one MRG32k3a stream seeded
+// `seed`, every query projected on the GPU; *sink = sum of the indices (the
+// CLI prints sink % 7), *ms = device time of the searches only.
+QT_API qt_status qt_bench_nn(uint64_t n, uint64_t queries, uint64_t seed, uint64_t* sink,
+                             double* ms) {
+  return guarded([&] {
+    if (n == 0 || queries == 0) raise(QT_ERR_INVALID_ARGUMENT, "bench-nn: n and queries must be >= 1");
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+      raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
+    QT_CUDA(cudaSetDevice(0));
+    const qt::SrcArgs a = make_src(0, QT_ENGINE_MRG32K3A, seed, 1, 1, nullptr, 0);
+    std::vector<void*> bufs;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    auto fin = [&] {
+      for (void* p : bufs) cudaFree(p);
+      if (e0) cudaEventDestroy(e0);
+      if (e1) cudaEventDestroy(e1);
+    };
+    try {
+      auto dalloc = [&](size_t b) {
+        void* p = nullptr;
+        QT_CUDA(cudaMalloc(&p, b));
+        bufs.push_back(p);
+        return p;
+      };
+      auto* dp = static_cast<double*>(dalloc(2 * n * 8));
+      auto* dq = static_cast<double*>(dalloc(2 * queries * 8));
+      auto* di = static_cast<unsigned long long*>(dalloc(queries * 8));
+      auto* ds = static_cast<unsigned long long*>(dalloc(8));
+      QT_CUDA(qt::launch_serial_normals(a, 0, 2 * n, dp, nullptr));
+      QT_CUDA(qt::launch_serial_normals(a, 2 * n, 2 * queries, dq, nullptr));
+      std::vector<double> hp(2 * n);
+      QT_CUDA(cudaMemcpy(hp.data(), dp, 2 * n * 8, cudaMemcpyDeviceToHost));
+      check_grid(2, n, hp.data(), 0);
+      double zeros[6] = {0, 0, 0, 0, 0, 0};
+      TableBlob tb = build_table(-1, 2, n, hp.data(), zeros, zeros, 0, 1, 1);
+      auto* dt = static_cast<uint8_t*>(dalloc(tb.hot.size()));
+      QT_CUDA(cudaMemcpy(dt, tb.hot.data(), tb.hot.size(), cudaMemcpyHostToDevice));
+      QT_CUDA(cudaMemset(ds, 0, 8));
+      QT_CUDA(cudaEventCreate(&e0));
+      QT_CUDA(cudaEventCreate(&e1));
+      QT_CUDA(cudaEventRecord(e0));
+      QT_CUDA(qt::launch_nearest(2, dt, static_cast<uint32_t>(tb.hot.size()), dq, queries, di, nullptr));
+      QT_CUDA(cudaEventRecord(e1));
+      QT_CUDA(qt::launch_sum_u64(di, queries, ds, nullptr));
+      g_launches.fetch_add(5);
+      unsigned long long s = 0;
+      QT_CUDA(cudaMemcpy(&s, ds, 8, cudaMemcpyDeviceToHost));
+      float t = 0;
+      QT_CUDA(cudaEventElapsedTime(&t, e0, e1));
+      if (sink) *sink = s;
+      if (ms) *ms = t;
+    } catch (...) {
+      fin();
+      throw;
+    }
+    fin();
+  });
+}
+
 QT_API qt_status qt_nearest(int32_t dim, uint64_t n_points, const double* points,
                             uint64_t n_queries, const double* queries, uint64_t* out) {
   return guarded([&] {

@@ -112,6 +112,10 @@ cudaError_t launch_lloyd_update(const double* X, const unsigned long long* cell,
                                 uint32_t* idx, uint32_t* key2, uint32_t* idx2, uint32_t* counts,
                                 uint32_t* offs, void* tmp, size_t tmp_bytes, cudaStream_t st);
 size_t lloyd_tmp_bytes(uint64_t M, uint64_t N);
+cudaError_t launch_pi(int engine, int skip, const SrcArgs& a, uint64_t samples, uint64_t streams,
+                      unsigned long long* inside, cudaStream_t st);
+cudaError_t launch_sum_u64(const unsigned long long* v, uint64_t n, unsigned long long* out,
+                           cudaStream_t st);
 cudaError_t launch_paths_x(int kind, bool resident, int P, const PathArgs& a, uint32_t blocks,
                            size_t smem, cudaStream_t st, int* bps);
 cudaError_t launch_paths_scan(int kind, int src, bool resident, int P, const ScanArgs& a,

@@ -440,6 +440,36 @@ def load_grid(path) -> QuantGrid:
     return QuantGrid(d.value, pts)
 
 
+# ---------------------------------------------------------------------------
+# micro-benchmarks (qtree_main.cpp bench-rng / bench-nn)
+# ---------------------------------------------------------------------------
+@dataclass
+class PiEstimate:
+    estimate: float
+    std_error: float
+    points: int
+    inside: int
+    ms: float
+
+
+def bench_pi(engine: int, seed: int, samples: int, streams: int = 1,
+             skip_ahead: bool = False) -> PiEstimate:
+    """estimate_pi_partitioned (monte_carlo.hpp:51-77) on the GPU."""
+    inside, est, se, ms = C.c_uint64(0), C.c_double(0), C.c_double(0), C.c_double(0)
+    _check(L.lib().qt_bench_pi(int(engine), int(seed), int(samples), int(streams),
+                               1 if skip_ahead else 0, C.byref(inside), C.byref(est),
+                               C.byref(se), C.byref(ms)), "bench_pi")
+    return PiEstimate(est.value, se.value, int(samples) // 2, inside.value, ms.value)
+
+
+def bench_nn(n: int, queries: int, seed: int = 12345) -> tuple[int, float]:
+    """(sum of nearest indices, device ms of the searches), qtree_main.cpp:162-191."""
+    sink, ms = C.c_uint64(0), C.c_double(0)
+    _check(L.lib().qt_bench_nn(int(n), int(queries), int(seed), C.byref(sink), C.byref(ms)),
+           "bench_nn")
+    return sink.value, ms.value
+
+
 def set_fast_path(enabled: bool) -> None:
     """Select the fast 1-D path (FP32 Box-Muller + certified cells + exact
     replay; identical counts) or the exact FP64 kernel for every path."""
