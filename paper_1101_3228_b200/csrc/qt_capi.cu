@@ -962,6 +962,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       if (const char* e = std::getenv("QT_X_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 4 ? 4 : 2;
       qt::PathArgs xa = a;
       xa.stages = 3u * p->max_tab <= 150u * 1024u ? 3u : 2u;
+      xa.probe_nored = std::getenv("QT_PROBE_NORED") ? 1u : 0u;
       const size_t xsmem = resident ? p->total_tab : static_cast<size_t>(xa.stages) * p->max_tab;
       int xbps = 1;
       QT_CUDA(qt::launch_paths_x(p->kind, resident, P, xa, 0, xsmem, st, &xbps));

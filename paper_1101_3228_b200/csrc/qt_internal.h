@@ -36,6 +36,7 @@ struct PathArgs {
   uint32_t resident_bytes;    // sum of table bytes (resident mode)
   uint32_t stages;            // shared-memory ring depth (power of 2, <= 8)
   uint32_t log_stages;
+  uint32_t probe_nored;       // diagnostics only (QT_PROBE_NORED): skip the count REDs
 };
 
 constexpr int kPathConsumers = 256;  // consumer threads per k_paths CTA

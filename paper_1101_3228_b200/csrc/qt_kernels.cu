@@ -398,7 +398,8 @@ struct ExactPath {
 template <int K, int P>
 __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act)[P],
                                             const uint8_t* tb, uint32_t k,
-                                            unsigned long long* joint, const uint8_t* gtables) {
+                                            unsigned long long* joint, const uint8_t* gtables,
+                                            bool count) {
   using C = Chain<K>;
   const LayerTable& h = *reinterpret_cast<const LayerTable*>(tb);
   const double x_safe = h.x_safe, lo = h.lo, inv_w = h.inv_w, nb_d = h.nb_d;
@@ -446,7 +447,7 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
     } else {  // exact scan over the cold block (NaN / inf / |x| >= x_safe)
       j = nearest_1d_scan(reinterpret_cast<const Rec1*>(gtables + h.cold_off), npts, x);
     }
-    if (act[p]) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + j, 1ull);
+    if (act[p] && count) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + j, 1ull);
     ps[p].i = j;
   }
 }
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_x(const __grid_constant_
       } else {
         mbar_wait_u32(full0 + 8u * s, ph);
       }
-      exact_layer<K, P>(ps, act, tb, k, a.joint, a.tables);
+      exact_layer<K, P>(ps, act, tb, k, a.joint, a.tables, a.probe_nored == 0);
       if constexpr (!RESIDENT) {
         named_barrier_sync(1, kFastThreads);  // every thread is done with stage s
         if (tid == 0 && g + S < steps_total) issue(g + S);
