@@ -38,8 +38,30 @@
 
 namespace qt {
 
+// The FP64 constants of both kernels. On the device they live in the constant
+// bank, so every DFMA takes them as a c[][] operand instead of rebuilding each
+// 64-bit literal with two uniform moves per use (ncu: UMOV was 12 % of the
+// path kernel's instructions); the host build reads the same values.
+#define QT_MATH_K_LIST                                                                  \
+  /* 0 */ 0x1.2492492492492p-3, -0x1.5555555555555p-3, 0x1.999999999999ap-3,          \
+  /* 3 */ 0x1.5555555555555p-2, kLn2Hi, kLn2Lo,                                        \
+  /* 6 */ -1.66666666666666324348e-01, 8.33333333332248946124e-03,                     \
+  /* 8 */ -1.98412698298579493134e-04, 2.75573137070700676789e-06,                     \
+  /* 10 */ -2.50507602534068634195e-08, 1.58969099521155010221e-10,                    \
+  /* 12 */ 4.16666666666666019037e-02, -1.38888888888741095749e-03,                    \
+  /* 14 */ 2.48015872894767294178e-05, -2.75573143513906633035e-07,                    \
+  /* 16 */ 2.08757232129817482790e-09, -1.13596475577881948265e-11,                    \
+  /* 18 */ 0x1.45f306dc9c883p-1, 0x1.921fb54442d18p+0, 0x1.1a62633145c07p-54,          \
+  /* 21 */ -0x1.f1976b7ed8fbcp-110, -0.125, -0.25, -0.5, 0.5, 1.0
 #if defined(__CUDACC__)
 static __device__ const LogEntry kLogTabDev[128] = {QT_LOGTAB_ENTRIES};
+static __constant__ double kMathKDev[] = {QT_MATH_K_LIST};
+#endif
+static const double kMathKHost[] = {QT_MATH_K_LIST};
+#if defined(__CUDA_ARCH__)
+#define QTK(i) (kMathKDev[i])
+#else
+#define QTK(i) (kMathKHost[i])
 #endif
 #if defined(__CUDA_ARCH__)
 QT_HD int64_t qt_bits(double x) { return __double_as_longlong(x); }
@@ -90,37 +112,33 @@ QT_HD double qt_log_unit(double u) {
   qt_logtab(i, &invc, &lhi, &llo);
   const double r = QT_FMA(m, invc, -1.0);
   const double kd = static_cast<double>(e);
-  const double t1 = QT_MUL(kd, kLn2Hi);               // exact (41-bit ln2 hi)
+  const double t1 = QT_MUL(kd, QTK(4));               // exact (41-bit ln2 hi)
   const double hi = QT_ADD(t1, lhi);
   const double lo_a = QT_ADD(QT_SUB(t1, hi), lhi);    // Fast2Sum (|t1| >= |lhi| or t1 = 0)
   const double hi2 = QT_ADD(hi, r);
   const double lo_b = QT_ADD(QT_SUB(hi, hi2), r);     // Fast2Sum (|hi| >= |r| or hi = 0)
   // log1p(r) - r = r^2 (-1/2 + r (1/3 + r (-1/4 + r (1/5 + r (-1/6 + r (1/7 - r/8))))))
-  const double p7 = QT_FMA(r, -0.125, 0x1.2492492492492p-3);
-  const double p6 = QT_FMA(r, p7, -0x1.5555555555555p-3);
-  const double p5 = QT_FMA(r, p6, 0x1.999999999999ap-3);
+  const double p7 = QT_FMA(r, QTK(22), QTK(0));
+  const double p6 = QT_FMA(r, p7, QTK(1));
+  const double p5 = QT_FMA(r, p6, QTK(2));
   const double p4 = QT_FMA(r, p5, -0.25);
-  const double p3 = QT_FMA(r, p4, 0x1.5555555555555p-2);
+  const double p3 = QT_FMA(r, p4, QTK(3));
   const double p2 = QT_FMA(r, p3, -0.5);
   const double tail = QT_MUL(QT_MUL(r, r), p2);
-  const double lo = QT_ADD(QT_ADD(QT_FMA(kd, kLn2Lo, llo), QT_ADD(lo_a, lo_b)), tail);
+  const double lo = QT_ADD(QT_ADD(QT_FMA(kd, QTK(5), llo), QT_ADD(lo_a, lo_b)), tail);
   return QT_ADD(hi2, lo);
 }
 
 QT_HD void qt_sincos_2pi(double a, double* s_out, double* c_out) {
   // fdlibm __kernel_sin / __kernel_cos coefficients (|x| <= pi/4)
-  const double S1 = -1.66666666666666324348e-01, S2 = 8.33333333332248946124e-03,
-               S3 = -1.98412698298579493134e-04, S4 = 2.75573137070700676789e-06,
-               S5 = -2.50507602534068634195e-08, S6 = 1.58969099521155010221e-10;
-  const double C1 = 4.16666666666666019037e-02, C2 = -1.38888888888741095749e-03,
-               C3 = 2.48015872894767294178e-05, C4 = -2.75573143513906633035e-07,
-               C5 = 2.08757232129817482790e-09, C6 = -1.13596475577881948265e-11;
-  const double q = QT_RINT(QT_MUL(a, 0x1.45f306dc9c883p-1));  // round(a * 2/pi)
-  const double t = QT_FMA(-q, 0x1.921fb54442d18p+0, a);       // exact
-  const double r = QT_FMA(-q, 0x1.1a62633145c07p-54, t);
+  const double S1 = QTK(6), S2 = QTK(7), S3 = QTK(8), S4 = QTK(9), S5 = QTK(10), S6 = QTK(11);
+  const double C1 = QTK(12), C2 = QTK(13), C3 = QTK(14), C4 = QTK(15), C5 = QTK(16),
+               C6 = QTK(17);
+  const double q = QT_RINT(QT_MUL(a, QTK(18)));  // round(a * 2/pi)
+  const double t = QT_FMA(-q, QTK(19), a);       // exact
+  const double r = QT_FMA(-q, QTK(20), t);
   // tail: (t - r) - q MID - q LO
-  const double y = QT_FMA(-q, -0x1.f1976b7ed8fbcp-110,
-                          QT_FMA(-q, 0x1.1a62633145c07p-54, QT_SUB(t, r)));
+  const double y = QT_FMA(-q, QTK(21), QT_FMA(-q, QTK(20), QT_SUB(t, r)));
   const double z = QT_MUL(r, r);
   const double v = QT_MUL(z, r);
   // sin(r + y) = r - ((z (y/2 - v P) - y) - v S1)
