@@ -1029,7 +1029,14 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
     const uint64_t cap = std::max<uint64_t>(1, M / (256 * 64));
     slices = std::min(slices, cap);
     slices = std::min<uint64_t>(slices, 1u << 30);
-    QT_CUDA(qt::launch_alg3(p->kind, src, a, static_cast<uint32_t>(slices), smem, st));
+    if (src == QT_ENGINE_MRG32K3A && (p->kind == QT_CHAIN_BROWNIAN_1D || p->kind == QT_CHAIN_OU_1D) &&
+        xkernel_enabled()) {
+      int P = 1;  // measured best for C3 (tools/alg3_probe.py)
+      if (const char* e = std::getenv("QT_X_P")) P = std::atoi(e) == 2 ? 2 : std::atoi(e) == 4 ? 4 : 1;
+      QT_CUDA(qt::launch_alg3_x(p->kind, P, a, static_cast<uint32_t>(slices), smem, st));
+    } else {
+      QT_CUDA(qt::launch_alg3(p->kind, src, a, static_cast<uint32_t>(slices), smem, st));
+    }
   }
   g_launches.fetch_add(1);
   return 1 + launches_before;

@@ -124,6 +124,8 @@ cudaError_t launch_paths_scan(int kind, int src, bool resident, int P, const Sca
 int paths_scan_blocks_per_sm(int kind, int src, bool resident, int P, size_t smem);
 cudaError_t launch_alg3(int kind, int src, const Alg3Args& a, uint32_t slices, size_t smem,
                         cudaStream_t st);
+cudaError_t launch_alg3_x(int kind, int P, const Alg3Args& a, uint32_t slices, size_t smem,
+                          cudaStream_t st);
 cudaError_t launch_finalize(bool alg3, const unsigned long long* joint, unsigned long long* visits,
                             double* pi, uint64_t samples, const FinalizeArgs& f, uint32_t n,
                             uint64_t max_cols, uint64_t max_rows, uint64_t max_elems,

@@ -672,6 +672,80 @@ __global__ void __launch_bounds__(kThreads) k_alg3(const Alg3Args a) {
 }
 
 // ---------------------------------------------------------------------------
+// k_alg3_x: Alg III for the 1-D chains with MRG32k3a (C3), k_alg3's arithmetic
+// bit for bit. A sample consumes exactly one Box-Muller pair (d + nps = 2:
+// z1 -> sample_marginal(k-1), z2 -> step), drawn with two interleaved MRG32k3a
+// steps; each thread keeps P samples in flight (contiguous sub-runs of its
+// slice) so the P dependency chains interleave. Tables k-1 and k stay in
+// shared memory for the CTA's lifetime.
+// ---------------------------------------------------------------------------
+template <int K, int P>
+__global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg3Args a) {
+  using C = Chain<K>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t k = blockIdx.y + 1;  // transition k-1 -> k
+  const uint64_t layer0 = static_cast<uint64_t>(k - 1) * a.M;
+  uint64_t lo = layer0 + a.M * blockIdx.x / gridDim.x;
+  uint64_t hi = layer0 + a.M * (blockIdx.x + 1) / gridDim.x;
+  lo = lo > a.first ? lo : a.first;
+  hi = hi < a.first + a.count ? hi : a.first + a.count;
+  if (lo >= hi) return;
+  const uint8_t* tk = smem;
+  const uint8_t* tp = smem + a.buf_bytes;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    const uint32_t bytes = a.tab_bytes[k - 1] + (k >= 2 ? a.tab_bytes[k - 2] : 0u);
+    mbar_expect_tx(&bar, bytes);
+    bulk_g2s(smem, a.tables + a.tab_off[k - 1], a.tab_bytes[k - 1], &bar);
+    if (k >= 2) bulk_g2s(smem + a.buf_bytes, a.tables + a.tab_off[k - 2], a.tab_bytes[k - 2], &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const LayerTable& hk = *reinterpret_cast<const LayerTable*>(tk);
+  const LayerTable& hp = *reinterpret_cast<const LayerTable*>(tp);
+  // the slice split over blockDim.x * P slots, slot v = tid * P + p
+  const uint64_t len = hi - lo, T = static_cast<uint64_t>(blockDim.x) * P;
+  const uint64_t q = len / T, rem = len % T;
+  Mrg st[P];
+  uint64_t cnt[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const uint64_t v = static_cast<uint64_t>(tid) * P + p;
+    cnt[p] = q + (v < rem ? 1u : 0u);
+    st[p] = Mrg{};
+    if (cnt[p]) {
+      Source<kSrcMrg> src;
+      src.start(a.src, lo + v * q + (v < rem ? v : rem));
+      st[p] = src.s;
+    }
+  }
+  const uint64_t rounds = q + (rem ? 1u : 0u);
+  unsigned long long* jl = a.joint + hk.joff;
+  const uint32_t npts = hk.n_pts;
+  for (uint64_t r = 0; r < rounds; ++r) {
+    double z1[P], z2[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      uint32_t u1, u2;
+      mrg_step2(st[p], u1, u2);
+      box_muller(mrg_to_unit(u1), mrg_to_unit(u2), z1[p], z2[p]);
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      double e0[1] = {z1[p]}, e1[1] = {z2[p]}, x[1], xn[1];
+      C::marginal(hk.marg_prev, k == 1, x, e0);  // sample_marginal(k-1, ...)
+      C::step(hk.step, x, xn, e1);               // step(k-1, ...)
+      const uint32_t i = k == 1 ? 0u : nearest_1d(hp, tp, x[0], a.tables);
+      const uint32_t j = nearest_1d(hk, tk, xn[0], a.tables);
+      if (r < cnt[p]) red_add_u64(jl + static_cast<uint64_t>(i) * npts + j, 1ull);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // finalize
 // ---------------------------------------------------------------------------
 // visits[k][j] = sum_i joint[k-1][i][j]  (grid.y = transition t = k-1)
@@ -933,6 +1007,21 @@ cudaError_t launch_alg3(int kind, int src, const Alg3Args& a, uint32_t slices, s
     case 2: return launch_alg3_s<2>(a, src, g, smem, st);
     default: return launch_alg3_s<3>(a, src, g, smem, st);
   }
+}
+
+// k_alg3_x (kind 0 = Brownian, 2 = OU; MRG32k3a), P samples in flight per thread
+cudaError_t launch_alg3_x(int kind, int P, const Alg3Args& a, uint32_t slices, size_t smem,
+                          cudaStream_t st) {
+  const dim3 g(slices, a.n);
+  auto go = [&](auto fn) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    fn<<<g, kThreads, smem, st>>>(a);
+    return cudaGetLastError();
+  };
+  if (kind == 0) return P == 1 ? go(k_alg3_x<0, 1>) : P == 4 ? go(k_alg3_x<0, 4>) : go(k_alg3_x<0, 2>);
+  return P == 1 ? go(k_alg3_x<2, 1>) : P == 4 ? go(k_alg3_x<2, 4>) : go(k_alg3_x<2, 2>);
 }
 
 cudaError_t launch_finalize(bool alg3, const unsigned long long* joint, unsigned long long* visits,

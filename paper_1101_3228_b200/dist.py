@@ -45,8 +45,16 @@ def estimate_distributed(kind, chain, grids, samples: int, engine=1, seed=12345,
     visits = torch.empty(plan.n_visits, dtype=torch.int64, device=joint.device)
     pi = torch.empty(plan.n_joint, dtype=torch.float64, device=joint.device)
     plan.finalize(kind, samples, joint, visits, pi)
-    v = visits.cpu().numpy().view(np.uint64)
-    j = joint.cpu().numpy().view(np.uint64)
-    p = pi.cpu().numpy()
+    # device -> pinned host (a pageable .cpu() of the 2 x 98 MB at C2 runs at a few GB/s)
+    hv = torch.empty(visits.shape, dtype=visits.dtype, pin_memory=True)
+    hj = torch.empty(joint.shape, dtype=joint.dtype, pin_memory=True)
+    hp = torch.empty(pi.shape, dtype=pi.dtype, pin_memory=True)
+    hv.copy_(visits, non_blocking=True)
+    hj.copy_(joint, non_blocking=True)
+    hp.copy_(pi, non_blocking=True)
+    torch.cuda.current_stream(joint.device).synchronize()
+    v = hv.numpy().view(np.uint64)
+    j = hj.numpy().view(np.uint64)
+    p = hp.numpy()
     x0 = QuantGrid(chain.dim(), np.zeros(chain.dim()))
     return QuantTree([x0] + list(grids), plan.sizes, v, j, p, samples)
