@@ -961,9 +961,25 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       int P = 2;
       if (const char* e = std::getenv("QT_X_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 4 ? 4 : 2;
       qt::PathArgs xa = a;
-      xa.stages = 3u * p->max_tab <= 150u * 1024u ? 3u : 2u;
+      // layers per pipeline stage (log_stages carries it: 1 or 2)
+      uint32_t Lp = 2;
+      if (const char* e = std::getenv("QT_X_L")) Lp = std::atoi(e) == 1 ? 1u : 2u;
+      uint32_t buf = p->max_tab;
+      if (Lp == 2)
+        for (int k = 0; k < p->n; k += 2) {
+          const int k1 = std::min(k + 1, p->n - 1);
+          buf = std::max<uint32_t>(buf, p->tab_off[k1] + p->tab_bytes[k1] - p->tab_off[k]);
+        }
+      if (Lp == 2 && 2ull * buf > 200u * 1024u) {  // two-layer stages do not fit: one layer
+        Lp = 1;
+        buf = p->max_tab;
+      }
+      xa.log_stages = Lp;
+      xa.buf_bytes = buf;
+      xa.stages = Lp == 2 ? 2u : (3u * p->max_tab <= 150u * 1024u ? 3u : 2u);
+      if (const char* e = std::getenv("QT_X_S")) xa.stages = std::max(2, std::min(8, std::atoi(e)));
       xa.probe_nored = std::getenv("QT_PROBE_NORED") ? 1u : 0u;
-      const size_t xsmem = resident ? p->total_tab : static_cast<size_t>(xa.stages) * p->max_tab;
+      const size_t xsmem = resident ? p->total_tab : static_cast<size_t>(xa.stages) * buf;
       int xbps = 1;
       QT_CUDA(qt::launch_paths_x(p->kind, resident, P, xa, 0, xsmem, st, &xbps));
       uint64_t xblocks = static_cast<uint64_t>(p->sm_count) * xbps;

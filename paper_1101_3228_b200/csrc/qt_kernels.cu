@@ -452,21 +452,27 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
   }
 }
 
-template <int K, bool RESIDENT, int P>
+// L = layers per pipeline stage: with L = 2 one stage holds the (contiguous)
+// tables of layers 2q+1 and 2q+2, which share one Box-Muller pair, so the table
+// wait and the barrier are paid once per two layers.
+template <int K, bool RESIDENT, int P, int L>
 __global__ void __launch_bounds__(kFastThreads) k_paths_x(const __grid_constant__ PathArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   const uint32_t tid = threadIdx.x;
   const uint32_t S = a.stages;
+  const uint32_t spr = (a.n + L - 1) / L;  // stage steps per round
   const uint64_t rounds = a.q + (a.rem ? 1u : 0u);
-  const uint64_t steps_total = rounds * a.n;
+  const uint64_t steps_total = rounds * spr;
   if (steps_total == 0) return;
   auto issue = [&](uint64_t g) {
-    const uint32_t k = static_cast<uint32_t>(g % a.n);
+    const uint32_t k0 = static_cast<uint32_t>(g % spr) * L;
+    const uint32_t k1 = min(k0 + L, a.n) - 1;
     const uint32_t st = static_cast<uint32_t>(g % S);
-    const uint32_t bytes = __ldg(a.tab_bytes + k);
+    const uint32_t off = __ldg(a.tab_off + k0);
+    const uint32_t bytes = __ldg(a.tab_off + k1) + __ldg(a.tab_bytes + k1) - off;
     mbar_expect_tx(&full[st], bytes);
-    bulk_g2s(smem + st * a.buf_bytes, a.tables + __ldg(a.tab_off + k), bytes, &full[st]);
+    bulk_g2s(smem + st * a.buf_bytes, a.tables + off, bytes, &full[st]);
   };
   if (tid == 0) {
     for (uint32_t s = 0; s < S; ++s) mbar_init(&full[s], 1);
@@ -510,13 +516,16 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_x(const __grid_constant_
       ps[p].x = 0.0;  // chains.hpp:43-46,81: the origin
       ps[p].i = 0;    // layer 0 is the singleton {x0}
     }
-    for (uint32_t k = 1; k <= a.n; ++k, ++g) {
+    for (uint32_t k = 1; k <= a.n; k += L, ++g) {
       if constexpr (RESIDENT) {
         tb = smem + (a.tab_off[k - 1] - a.tab_off[0]);
       } else {
         mbar_wait_u32(full0 + 8u * s, ph);
       }
       exact_layer<K, P>(ps, act, tb, k, a.joint, a.tables, a.probe_nored == 0);
+      if (L == 2 && k + 1 <= a.n)
+        exact_layer<K, P>(ps, act, tb + __ldg(a.tab_bytes + k - 1), k + 1, a.joint, a.tables,
+                          a.probe_nored == 0);
       if constexpr (!RESIDENT) {
         named_barrier_sync(1, kFastThreads);  // every thread is done with stage s
         if (tid == 0 && g + S < steps_total) issue(g + S);
@@ -534,7 +543,7 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_x(const __grid_constant_
 template <int K, bool RES, int P>
 static cudaError_t launch_x_t(const PathArgs& a, uint32_t blocks, size_t smem, cudaStream_t st,
                               int* bps) {
-  auto fn = k_paths_x<K, RES, P>;
+  auto fn = a.log_stages == 2 ? k_paths_x<K, RES, P, 2> : k_paths_x<K, RES, P, 1>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;

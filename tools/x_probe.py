@@ -14,9 +14,12 @@ ch = q.BrownianChain1d(50)
 plan = Plan(ch, q.build_brownian_grids(ch, N), 0)
 print(f"n=50 N={N}: joint {plan.n_joint * 8 / 1e6:.1f} MB")
 ref = None
-for name, env in (("k_paths", {"QT_XKERNEL": "0"}), ("x P=1", {"QT_X_P": "1"}),
-                  ("x P=2", {"QT_X_P": "2"}), ("x P=4", {"QT_X_P": "4"})):
-    for k in ("QT_XKERNEL", "QT_X_P"):
+cases = (("k_paths", {"QT_XKERNEL": "0"}), ("x P=1 L=1", {"QT_X_P": "1", "QT_X_L": "1"}),
+         ("x P=2 L=1", {"QT_X_P": "2", "QT_X_L": "1"}), ("x P=2 L=2", {"QT_X_P": "2", "QT_X_L": "2"}),
+         ("x P=2 L=2 S=3", {"QT_X_P": "2", "QT_X_L": "2", "QT_X_S": "3"}),
+         ("x P=1 L=2", {"QT_X_P": "1", "QT_X_L": "2"}), ("x P=4 L=2", {"QT_X_P": "4", "QT_X_L": "2"}))
+for name, env in cases:
+    for k in ("QT_XKERNEL", "QT_X_P", "QT_X_L", "QT_X_S"):
         os.environ.pop(k, None)
     os.environ.update(env)
     joint = plan.zeros_joint()
