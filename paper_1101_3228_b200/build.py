@@ -51,13 +51,19 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
+    import fcntl
     os.makedirs(LIB_DIR, exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-o", tmp, *sources(), "-ldl"]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    # one builder at a time (torchrun starts one process per GPU, each may call build())
+    with open(os.path.join(LIB_DIR, ".build.lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if not force and up_to_date():
+            return LIB
+        tmp = f"{LIB}.tmp{os.getpid()}"
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-o", tmp, *sources(), "-ldl"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, LIB)
     return LIB
 
 
