@@ -287,8 +287,8 @@ def run_ours(args, rank, world, local_rank):
         ev[1].record(st)
         plan.count(est, 1, 12345, first, count, units, joint)
         ev[2].record(st)
-        if world > 1:
-            dist.reduce(joint, dst=0, op=dist.ReduceOp.SUM)
+        if world > 1:  # the one exchange step: an all-reduce of the int64 counts
+            dist.all_reduce(joint, op=dist.ReduceOp.SUM)
         if rank == 0:
             plan.finalize(est, M, joint, visits, pi)
         ev[3].record(st)
@@ -387,7 +387,7 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic: MRG32k3a seed 12345 paths on the reference's Lloyd grids",
         "config": {"workload": text, "n": n, "N": N, "M": M,
                    "estimator": ["AlgI", "AlgII", "AlgIII"][est], "engine": "mrg32k3a",
-                   "parallelism": f"paths sharded over {world} GPU(s), one NCCL reduce",
+                   "parallelism": f"paths sharded over {world} GPU(s), one NCCL all-reduce",
                    "l2": "flushed between timed steps (256 MiB write)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
@@ -437,6 +437,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and os.environ.get("QT_BENCH_SHARE_GPU"):  # test hook: all ranks on one GPU
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank)
         return
@@ -444,7 +446,11 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("QT_BENCH_DIST_BACKEND", "nccl")  # gloo: test hook only
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:

@@ -3,7 +3,7 @@
 Paths are sharded exactly like the reference's Algorithm II workers,
 [M g / G, M (g+1) / G) (estimate.hpp:180-181); each rank counts its shard with
 the fused path kernel into a private int64 joint matrix, and a single NCCL
-reduce (sum) to rank 0 replaces CountMatrixSet::add (quant_tree.hpp:35-40).
+all-reduce (sum) replaces CountMatrixSet::add (quant_tree.hpp:35-40).
 Counts are bit-identical for any world size because every path's stream is
 positioned by its global index (stream.hpp:190-199) and integer sums are
 associative.
@@ -39,7 +39,7 @@ def estimate_distributed(kind, chain, grids, samples: int, engine=1, seed=12345,
     joint = plan.zeros_joint()
     plan.count(kind, engine, seed, first, count, units, joint)
     if world > 1:
-        dist.reduce(joint, dst=0, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(joint, op=dist.ReduceOp.SUM, group=group)
     if rank != 0:
         return None
     visits = torch.empty(plan.n_visits, dtype=torch.int64, device=joint.device)
