@@ -709,6 +709,7 @@ struct qt_plan {
   uint32_t* d_ftab_off = nullptr;
   uint32_t* d_ftab_bytes = nullptr;
   uint32_t max_ftab = 0, total_ftab = 0;
+  std::vector<uint32_t> ftab_off_h, ftab_bytes_h;
   uint64_t amb_cap = 0, fast_paths = 0;
 
   ~qt_plan() {
@@ -805,6 +806,8 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
       ftables.insert(ftables.end(), b.fast.begin(), b.fast.end());
     }
     p->total_ftab = static_cast<uint32_t>(ftables.size());
+    p->ftab_off_h = foff;
+    p->ftab_bytes_h = fbytes;
     if (std::getenv("QT_DEBUG"))
       std::fprintf(stderr, "qtree: fast tables max %u B, total %u B\n", p->max_ftab, p->total_ftab);
   }
@@ -933,9 +936,15 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       if (const char* e = std::getenv("QT_FAST_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 2 ? 2 : 4;
       // fast tables: all resident when they fit, else prefetched S layers ahead
       const bool fres = p->total_ftab <= kResidentBudget;
-      uint32_t st_n = 3;
+      // stages of two layers (k_paths_fast pairs the layers of one Box-Muller draw)
+      uint32_t fbuf = p->max_ftab;
+      for (int k = 0; k < p->n; k += 2) {
+        const int k1 = std::min(k + 1, p->n - 1);
+        fbuf = std::max<uint32_t>(fbuf, p->ftab_off_h[k1] + p->ftab_bytes_h[k1] - p->ftab_off_h[k]);
+      }
+      uint32_t st_n = 2;
       if (const char* e = std::getenv("QT_FAST_STAGES")) st_n = std::max(2, std::min(8, std::atoi(e)));
-      const size_t fsmem = fres ? p->total_ftab : static_cast<size_t>(st_n) * p->max_ftab;
+      const size_t fsmem = fres ? p->total_ftab : static_cast<size_t>(st_n) * fbuf;
       qt::PathArgs fa_args = a;
       const int bps = qt::paths_fast_blocks_per_sm(p->kind, fres, P, fsmem);
       uint64_t blocks = static_cast<uint64_t>(p->sm_count) * bps;
@@ -946,7 +955,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       fa_args.q = count / T;
       fa_args.rem = count % T;
       qt::FastArgs fa{fa_args, p->d_amb, p->d_stats, std::min(p->amb_cap, want),
-                      p->d_ftables, p->d_ftab_off, p->d_ftab_bytes, p->max_ftab, p->total_ftab,
+                      p->d_ftables, p->d_ftab_off, p->d_ftab_bytes, fbuf, p->total_ftab,
                       st_n, {}, std::getenv("QT_PROBE_NORED") ? 1u : 0u};
       mrg_back_jump(2 * ((static_cast<uint64_t>(p->n) + 1) / 2), fa.back);
       QT_CUDA(cudaMemsetAsync(p->d_stats, 0, sizeof(unsigned long long), st));

@@ -282,17 +282,21 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_fast(const __grid_consta
   __shared__ __align__(8) uint64_t full[kMaxStages];
   const uint32_t tid = threadIdx.x;
   const uint32_t S = f.fstages;
+  constexpr uint32_t L = 2;  // layers per stage: the pair sharing one Box-Muller draw
+  const uint32_t spr = (a.n + L - 1) / L;
   const uint64_t rounds = a.q + (a.rem ? 1u : 0u);
-  const uint64_t steps_total = rounds * a.n;
+  const uint64_t steps_total = rounds * spr;
   if (steps_total == 0) return;
 
-  // issue the table of global layer step g into its stage (thread 0 only)
+  // issue the tables of global stage step g into its stage (thread 0 only)
   auto issue = [&](uint64_t g) {
-    const uint32_t k = static_cast<uint32_t>(g % a.n);
+    const uint32_t k0 = static_cast<uint32_t>(g % spr) * L;
+    const uint32_t k1 = min(k0 + L, a.n) - 1;
     const uint32_t st = static_cast<uint32_t>(g % S);
-    const uint32_t bytes = __ldg(f.ftab_bytes + k);
+    const uint32_t off = __ldg(f.ftab_off + k0);
+    const uint32_t bytes = __ldg(f.ftab_off + k1) + __ldg(f.ftab_bytes + k1) - off;
     mbar_expect_tx(&full[st], bytes);
-    bulk_g2s(smem + st * f.fbuf_bytes, f.ftables + __ldg(f.ftab_off + k), bytes, &full[st]);
+    bulk_g2s(smem + st * f.fbuf_bytes, f.ftables + off, bytes, &full[st]);
   };
   if (tid == 0) {
     for (uint32_t s = 0; s < S; ++s) mbar_init(&full[s], 1);
@@ -337,13 +341,16 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_fast(const __grid_consta
       ps[p].i = 0;
       ps[p].amb_k = 0;
     }
-    for (uint32_t k = 1; k <= a.n; ++k, ++g) {
+    for (uint32_t k = 1; k <= a.n; k += L, ++g) {
       if constexpr (RESIDENT) {
         tb = smem + f.ftab_off[k - 1];
       } else {
         mbar_wait_u32(full0 + 8u * s, ph);
       }
       fast_layer<K, P>(ps, act, tb, k, a.joint, f.probe_nored == 0);
+      if (k + 1 <= a.n)
+        fast_layer<K, P>(ps, act, tb + __ldg(f.ftab_bytes + k - 1), k + 1, a.joint,
+                         f.probe_nored == 0);
       if constexpr (!RESIDENT) {
         named_barrier_sync(1, kFastThreads);  // every thread is done with stage s
         if (tid == 0 && g + S < steps_total) issue(g + S);
