@@ -1006,14 +1006,17 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
     if (p->d_stables && scan_enabled()) {  // d >= 2: FP32 scan + exact FP64 decision
       // queries per thread: d = 2 keeps two CTAs per SM at P = 2; d = 3 is one
       // CTA per SM anyway (64 KB tables), where P = 4 gives the ILP
-      int P = p->dim == 2 ? 2 : 4;
+      // queries per thread: 2 (d = 2: three 256-thread CTAs per SM; d = 3: one
+      // 512-thread CTA per SM, the 64 KB tables allow no more)
+      int P = 2;
       if (const char* e = std::getenv("QT_SCAN_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 2 ? 2 : 4;
+      const uint64_t nt = p->dim == 3 ? 512 : 256;  // scan_threads<K>() in qt_scan.cu
       const bool sres = p->total_stab <= kResidentBudget;
       const uint32_t S = 3u * p->max_stab <= 200u * 1024u ? 3u : 2u;
       const size_t ssmem = sres ? p->total_stab : static_cast<size_t>(S) * p->max_stab;
       const int sbps = qt::paths_scan_blocks_per_sm(p->kind, src, sres, P, ssmem);
       uint64_t sblocks = static_cast<uint64_t>(p->sm_count) * sbps;
-      const uint64_t per_block = 256ull * P;
+      const uint64_t per_block = nt * P;
       const uint64_t sneed = (count + per_block - 1) / per_block;
       if (sneed < sblocks) sblocks = sneed;
       const uint64_t T = sblocks * per_block;

@@ -29,7 +29,9 @@
 
 namespace qt {
 
-constexpr int kScanThreads = 256;
+// threads per CTA: d = 3 tables are 64 KB, so one CTA per SM; it gets 16 warps
+template <int K>
+__host__ __device__ constexpr int scan_threads() { return Chain<K>::D == 3 ? 512 : 256; }
 constexpr int kScanMaxStages = 4;
 
 // {s, s} * b + c on the FP32x2 pipe (SASS FFMA2 with a broadcast scalar)
@@ -257,7 +259,10 @@ __device__ __forceinline__ void scan_project(const uint8_t* tb, const uint8_t* x
 }
 
 template <int K, int SRC, bool RESIDENT, int P>
-__global__ void __launch_bounds__(kScanThreads, P >= 4 ? 1 : 2) k_paths_scan(const __grid_constant__ ScanArgs f) {
+#ifndef QT_SCAN_MINB2
+#define QT_SCAN_MINB2 3
+#endif
+__global__ void __launch_bounds__(scan_threads<K>(), (P >= 4 || Chain<K>::D == 3) ? 1 : QT_SCAN_MINB2) k_paths_scan(const __grid_constant__ ScanArgs f) {
   using C = Chain<K>;
   constexpr int D = C::D;
   const PathArgs& a = f.p;
@@ -290,7 +295,8 @@ __global__ void __launch_bounds__(kScanThreads, P >= 4 ? 1 : 2) k_paths_scan(con
   __syncthreads();
 
   // P slots per thread, slot v = gid P + p owns a contiguous run of paths
-  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * kScanThreads + tid;
+  constexpr uint32_t kNT = scan_threads<K>();
+  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * kNT + tid;
   Source<SRC> src[P];
   uint64_t beg[P], cnt[P];
 #pragma unroll
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(kScanThreads, P >= 4 ? 1 : 2) k_paths_scan(con
         }
       }
       if constexpr (!RESIDENT) {
-        named_barrier_sync(1, kScanThreads);  // every thread is done with stage s
+        named_barrier_sync(1, kNT);  // every thread is done with stage s
         if (tid == 0 && g + S < steps_total) issue(g + S);
         tb += f.sbuf_bytes;
         if (++s == S) {
@@ -362,7 +368,7 @@ static cudaError_t launch_scan_t(const ScanArgs& a, uint32_t blocks, size_t smem
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  fn<<<blocks, kScanThreads, smem, st>>>(a);
+  fn<<<blocks, scan_threads<K>(), smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -371,7 +377,7 @@ static int scan_bps_t(size_t smem) {
   auto fn = k_paths_scan<K, SRC, RES, P>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kScanThreads, smem) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, scan_threads<K>(), smem) != cudaSuccess)
     return 1;
   return nb > 0 ? nb : 1;
 }
