@@ -1146,7 +1146,7 @@ void d2h_pinned(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   QT_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
   QT_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
   auto par_copy = [](uint8_t* d, const uint8_t* s, size_t n) {
-    constexpr int kT = 4;
+    constexpr int kT = 8;
     std::vector<std::thread> th;
     const size_t per = (n + kT - 1) / kT;
     for (int t = 1; t < kT; ++t) {
