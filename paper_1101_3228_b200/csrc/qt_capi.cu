@@ -909,7 +909,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
     a.buf_bytes = p->max_tab;
     a.resident_bytes = p->total_tab;
     a.stages = p->stages;
-    a.log_stages = 0;
+    a.layers_per_stage = 1;
     const bool resident = p->total_tab <= kResidentBudget;
     const size_t smem = resident ? p->total_tab : static_cast<size_t>(p->stages) * p->max_tab;
     const bool fast = fast_enabled() && src == QT_ENGINE_MRG32K3A && p->d_ftables &&
@@ -970,7 +970,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       int P = 2;
       if (const char* e = std::getenv("QT_X_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 4 ? 4 : 2;
       qt::PathArgs xa = a;
-      // layers per pipeline stage (log_stages carries it: 1 or 2)
+      // layers per pipeline stage (1 or 2)
       uint32_t Lp = 2;
       if (const char* e = std::getenv("QT_X_L")) Lp = std::atoi(e) == 1 ? 1u : 2u;
       uint32_t buf = p->max_tab;
@@ -983,7 +983,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
         Lp = 1;
         buf = p->max_tab;
       }
-      xa.log_stages = Lp;
+      xa.layers_per_stage = Lp;
       xa.buf_bytes = buf;
       xa.stages = Lp == 2 ? 2u : (3u * p->max_tab <= 150u * 1024u ? 3u : 2u);
       if (const char* e = std::getenv("QT_X_S")) xa.stages = std::max(2, std::min(8, std::atoi(e)));
@@ -1051,6 +1051,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
     a.count = count;
     a.n = static_cast<uint32_t>(p->n);
     a.buf_bytes = p->max_tab;
+    a.probe_nored = std::getenv("QT_PROBE_NORED") ? 1u : 0u;
     const size_t smem = 2ull * p->max_tab;
     // slices per layer: ~8 waves of resident CTAs overall, >= 64 samples per thread
     uint64_t slices = std::max<uint64_t>(1, (static_cast<uint64_t>(p->sm_count) * 32) / p->n);

@@ -35,7 +35,7 @@ struct PathArgs {
   uint32_t buf_bytes;         // staging buffer size (max table bytes)
   uint32_t resident_bytes;    // sum of table bytes (resident mode)
   uint32_t stages;            // shared-memory ring depth (power of 2, <= 8)
-  uint32_t log_stages;
+  uint32_t layers_per_stage;  // k_paths_x: layer tables per pipeline stage (1 or 2)
   uint32_t probe_nored;       // diagnostics only (QT_PROBE_NORED): skip the count REDs
 };
 
@@ -85,6 +85,7 @@ struct Alg3Args {
   uint64_t first, count;  // unit window within [0, n M)
   uint32_t n;
   uint32_t buf_bytes;
+  uint32_t probe_nored;   // diagnostics only (QT_PROBE_NORED): skip the count REDs
 };
 
 struct FinalizeArgs {

@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_x(const __grid_constant_
 template <int K, bool RES, int P>
 static cudaError_t launch_x_t(const PathArgs& a, uint32_t blocks, size_t smem, cudaStream_t st,
                               int* bps) {
-  auto fn = a.log_stages == 2 ? k_paths_x<K, RES, P, 2> : k_paths_x<K, RES, P, 1>;
+  auto fn = a.layers_per_stage == 2 ? k_paths_x<K, RES, P, 2> : k_paths_x<K, RES, P, 1>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg
       C::step(hk.step, x, xn, e1);               // step(k-1, ...)
       const uint32_t i = k == 1 ? 0u : nearest_1d(hp, tp, x[0], a.tables);
       const uint32_t j = nearest_1d(hk, tk, xn[0], a.tables);
-      if (r < cnt[p]) red_add_u64(jl + static_cast<uint64_t>(i) * npts + j, 1ull);
+      if (r < cnt[p] && !a.probe_nored) red_add_u64(jl + static_cast<uint64_t>(i) * npts + j, 1ull);
     }
   }
 }
