@@ -446,12 +446,19 @@ std::vector<uint8_t> build_fast_table(int kind, const std::vector<double>& t,
     std::nth_element(mags.begin(), mags.begin() + mags.size() / 2, mags.end());
     const double scale = std::max(mags[mags.size() / 2] / 0.6745, 1e-300);  // ~ sd of the cells
     uint32_t best = 0;
+    std::vector<double> u(N - 1);
     for (double q : {0.0, 0.03, 0.06, 0.1, 0.15, 0.22, 0.3}) {
       const double g = q / (scale * scale);
-      const double u0 = qt::fmap_g(t[0], g), u1 = qt::fmap_g(t[N - 2], g);
+      for (uint64_t c = 0; c + 1 < N; ++c) u[c] = qt::fmap_g(t[c], g);
+      const double u0 = u[0], u1 = u[N - 2];
       if (!(u1 > u0) || !std::isfinite(u1 - u0)) continue;
-      for (uint32_t m4 = 4; m4 <= 32; ++m4) {  // nb = m4/4 N
-        const uint32_t cand = static_cast<uint32_t>((static_cast<uint64_t>(m4) * N + 3) / 4);
+      // one threshold per bucket needs a bucket width below the smallest gap
+      double gap = u1 - u0;
+      for (uint64_t c = 1; c + 1 < N; ++c) gap = std::min(gap, u[c] - u[c - 1]);
+      if (!(gap > 0.0)) continue;
+      double want = std::ceil((u1 - u0) / gap) + 1.0;
+      for (int tries = 0; tries < 8 && want <= 8.0 * N; ++tries, want = std::ceil(want * 1.02) + 1) {
+        const uint32_t cand = static_cast<uint32_t>(want);
         if (best && cand >= best) break;
         const double a = cand / (u1 - u0), bb = -u0 * a;
         uint32_t prev = 0xFFFFFFFFu, worst = 0, run = 0;
