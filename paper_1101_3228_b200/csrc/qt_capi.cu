@@ -1438,6 +1438,40 @@ QT_API qt_status qt_plan_finalize(qt_plan* plan, int32_t estimator, uint64_t sam
   });
 }
 
+// Device tables of one grid for batch projection: the exact table (+ cold
+// block) and, for d >= 2, the FP32 scan table behind it. Uploads into *buf
+// (grown as needed) and enqueues the projection of nq device queries.
+struct GridTables {
+  std::vector<uint8_t> blob;  // exact hot | exact cold | scan (d >= 2)
+  uint32_t hot_bytes = 0, scan_off = 0, scan_bytes = 0;
+};
+// d >= 2 grids this small are faster with the plain FP64 scan (k_nearest)
+constexpr uint64_t kScanMinPoints = 192;
+
+GridTables grid_tables(int dim, uint64_t n, const double* pts) {
+  double zeros[6] = {0, 0, 0, 0, 0, 0};
+  TableBlob tb = build_table(-1, dim, n, pts, zeros, zeros, 0, 1, 1);
+  GridTables g;
+  g.blob = tb.hot;
+  g.hot_bytes = static_cast<uint32_t>(tb.hot.size());
+  set_cold_off(g.blob, g.blob.size());
+  g.blob.insert(g.blob.end(), tb.cold.begin(), tb.cold.end());
+  if (dim >= 2 && n >= kScanMinPoints) {
+    g.blob.resize(round16(g.blob.size()), 0);
+    g.scan_off = static_cast<uint32_t>(g.blob.size());
+    const auto sc = build_scan_table(dim, n, pts, zeros, 0, 0);
+    g.scan_bytes = static_cast<uint32_t>(sc.size());
+    g.blob.insert(g.blob.end(), sc.begin(), sc.end());
+  }
+  return g;
+}
+cudaError_t project_on_device(int dim, const GridTables& g, const uint8_t* d_blob, const double* dq,
+                              uint64_t nq, unsigned long long* dout, cudaStream_t st) {
+  if (dim >= 2 && g.scan_bytes && g.scan_bytes <= 200u * 1024u)
+    return qt::launch_nearest_scan(dim, d_blob + g.scan_off, g.scan_bytes, d_blob, dq, nq, dout, st);
+  return qt::launch_nearest(dim, d_blob, g.hot_bytes, dq, nq, dout, st);
+}
+
 // lloyd_build (lloyd.hpp:59-107) with the GaussianSampler on the serial
 // MRG32k3a stream seeded `stream_seed` (the pipeline passes seed ^ 0x9E3779B9,
 // pipeline.hpp:35,63). normals (nullable): the stream's normals supplied by the
@@ -1530,19 +1564,15 @@ QT_API qt_status qt_lloyd_build(int32_t dim, uint64_t n_points, int32_t iteratio
         for (int it = 0; it < iterations; ++it) {
           // snapshot grid (lloyd.hpp:88-89): the reference's QuantGrid checks
           check_grid(dim, N, c.data(), 0);
-          double zeros[6] = {0, 0, 0, 0, 0, 0};
-          TableBlob tb = build_table(-1, dim, N, c.data(), zeros, zeros, 0, 1, 1);
-          std::vector<uint8_t> t = tb.hot;
-          const uint32_t hot_bytes = static_cast<uint32_t>(t.size());
-          set_cold_off(t, t.size());
-          t.insert(t.end(), tb.cold.begin(), tb.cold.end());
+          const GridTables gt = grid_tables(dim, N, c.data());
+          const std::vector<uint8_t>& t = gt.blob;
           if (t.size() > dT_bytes) {
             dT = static_cast<uint8_t*>(dalloc(t.size()));
             dT_bytes = t.size();
           }
           QT_CUDA(cudaMemcpyAsync(dT, t.data(), t.size(), cudaMemcpyHostToDevice, st));
           fetch(dX, M * d);
-          QT_CUDA(qt::launch_nearest(dim, dT, hot_bytes, dX, M, dcell, st));
+          QT_CUDA(project_on_device(dim, gt, dT, dX, M, dcell, st));
           QT_CUDA(qt::launch_lloyd_update(dX, dcell, M, N, dim, dC, dd2, key, idx, key2, idx2, cnt,
                                           offs, tmp, tmp_bytes, st));
           g_launches.fetch_add(4);
@@ -1653,15 +1683,14 @@ QT_API qt_status qt_bench_nn(uint64_t n, uint64_t queries, uint64_t seed, uint64
       std::vector<double> hp(2 * n);
       QT_CUDA(cudaMemcpy(hp.data(), dp, 2 * n * 8, cudaMemcpyDeviceToHost));
       check_grid(2, n, hp.data(), 0);
-      double zeros[6] = {0, 0, 0, 0, 0, 0};
-      TableBlob tb = build_table(-1, 2, n, hp.data(), zeros, zeros, 0, 1, 1);
-      auto* dt = static_cast<uint8_t*>(dalloc(tb.hot.size()));
-      QT_CUDA(cudaMemcpy(dt, tb.hot.data(), tb.hot.size(), cudaMemcpyHostToDevice));
+      const GridTables gt = grid_tables(2, n, hp.data());
+      auto* dt = static_cast<uint8_t*>(dalloc(gt.blob.size()));
+      QT_CUDA(cudaMemcpy(dt, gt.blob.data(), gt.blob.size(), cudaMemcpyHostToDevice));
       QT_CUDA(cudaMemset(ds, 0, 8));
       QT_CUDA(cudaEventCreate(&e0));
       QT_CUDA(cudaEventCreate(&e1));
       QT_CUDA(cudaEventRecord(e0));
-      QT_CUDA(qt::launch_nearest(2, dt, static_cast<uint32_t>(tb.hot.size()), dq, queries, di, nullptr));
+      QT_CUDA(project_on_device(2, gt, dt, dq, queries, di, nullptr));
       QT_CUDA(cudaEventRecord(e1));
       QT_CUDA(qt::launch_sum_u64(di, queries, ds, nullptr));
       g_launches.fetch_add(5);
@@ -1690,12 +1719,8 @@ QT_API qt_status qt_nearest(int32_t dim, uint64_t n_points, const double* points
     int avail = 0;
     if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
       raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
-    double zeros[6] = {0, 0, 0, 0, 0, 0};
-    TableBlob tb = build_table(-1, dim, n_points, points, zeros, zeros, 0, 1, 1);
-    std::vector<uint8_t> t = tb.hot;
-    const uint32_t hot_bytes = static_cast<uint32_t>(t.size());
-    set_cold_off(t, t.size());
-    t.insert(t.end(), tb.cold.begin(), tb.cold.end());
+    const GridTables gt = grid_tables(dim, n_points, points);
+    const std::vector<uint8_t>& t = gt.blob;
     QT_CUDA(cudaSetDevice(0));
     uint8_t* d_t = nullptr;
     double* d_q = nullptr;
@@ -1711,7 +1736,7 @@ QT_API qt_status qt_nearest(int32_t dim, uint64_t n_points, const double* points
       QT_CUDA(cudaMalloc(&d_o, n_queries * sizeof(uint64_t)));
       QT_CUDA(cudaMemcpy(d_t, t.data(), t.size(), cudaMemcpyHostToDevice));
       QT_CUDA(cudaMemcpy(d_q, queries, n_queries * dim * sizeof(double), cudaMemcpyHostToDevice));
-      QT_CUDA(qt::launch_nearest(dim, d_t, hot_bytes, d_q, n_queries, d_o, nullptr));
+      QT_CUDA(project_on_device(dim, gt, d_t, d_q, n_queries, d_o, nullptr));
       g_launches.fetch_add(1);
       QT_CUDA(cudaMemcpy(out, d_o, n_queries * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     } catch (...) {

@@ -123,6 +123,9 @@ cudaError_t launch_paths_x(int kind, bool resident, int P, const PathArgs& a, ui
 cudaError_t launch_paths_scan(int kind, int src, bool resident, int P, const ScanArgs& a,
                               uint32_t blocks, size_t smem, cudaStream_t st);
 int paths_scan_blocks_per_sm(int kind, int src, bool resident, int P, size_t smem);
+cudaError_t launch_nearest_scan(int dim, const uint8_t* stable, uint32_t sbytes,
+                                const uint8_t* xtable, const double* q, uint64_t nq,
+                                unsigned long long* out, cudaStream_t st);
 cudaError_t launch_alg3(int kind, int src, const Alg3Args& a, uint32_t slices, size_t smem,
                         cudaStream_t st);
 cudaError_t launch_alg3_x(int kind, int P, const Alg3Args& a, uint32_t slices, size_t smem,

@@ -362,6 +362,62 @@ __global__ void __launch_bounds__(scan_threads<K>(), (P >= 4 || Chain<K>::D == 3
   }
 }
 
+// Batch K2 (NnIndex::nearest over many queries, nn.hpp:150-167) for d >= 2:
+// the scan table staged once per CTA, P queries per thread, scan_project's
+// exact decision. Loops are warp-uniform (scan_project's rescan is
+// warp-cooperative); out-of-range slots query point 0 and are discarded.
+// `xtable` is the layer's exact table (LayerTable + FP64 points); the scan
+// table's exact_off is relative to it (0).
+template <int D, int P>
+__global__ void __launch_bounds__(256) k_nearest_scan(const uint8_t* stable, uint32_t sbytes,
+                                                      const uint8_t* xtable, const double* q,
+                                                      uint64_t nq, unsigned long long* out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, sbytes);
+    bulk_g2s(smem, stable, sbytes, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const uint64_t per_iter = static_cast<uint64_t>(gridDim.x) * blockDim.x * P;
+  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x * P; base < nq;
+       base += per_iter) {
+    double x[P][D];
+    uint64_t qi[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      qi[p] = base + static_cast<uint64_t>(threadIdx.x) * P + p;
+      const uint64_t src = qi[p] < nq ? qi[p] : 0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) x[p][c] = q[src * D + c];
+    }
+    uint32_t cell[P];
+    scan_project<D, P>(smem, xtable, x, cell);
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+      if (qi[p] < nq) out[qi[p]] = cell[p];
+  }
+}
+
+cudaError_t launch_nearest_scan(int dim, const uint8_t* stable, uint32_t sbytes,
+                                const uint8_t* xtable, const double* q, uint64_t nq,
+                                unsigned long long* out, cudaStream_t st) {
+  constexpr int P = 2;
+  const uint64_t want = (nq + 256 * P - 1) / (256 * P);
+  const uint32_t blocks = static_cast<uint32_t>(want < 148u * 4u ? (want ? want : 1) : 148u * 4u);
+  auto go = [&](auto fn) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sbytes));
+    if (e != cudaSuccess) return e;
+    fn<<<blocks, 256, sbytes, st>>>(stable, sbytes, xtable, q, nq, out);
+    return cudaGetLastError();
+  };
+  return dim == 2 ? go(k_nearest_scan<2, P>) : go(k_nearest_scan<3, P>);
+}
+
 template <int K, int SRC, bool RES, int P>
 static cudaError_t launch_scan_t(const ScanArgs& a, uint32_t blocks, size_t smem, cudaStream_t st) {
   auto fn = k_paths_scan<K, SRC, RES, P>;
