@@ -1070,6 +1070,10 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       int P = 1;  // measured best for C3 (tools/alg3_probe.py)
       if (const char* e = std::getenv("QT_X_P")) P = std::atoi(e) == 2 ? 2 : std::atoi(e) == 4 ? 4 : 1;
       QT_CUDA(qt::launch_alg3_x(p->kind, P, a, static_cast<uint32_t>(slices), smem, st));
+    } else if (p->d_stables && scan_enabled() && 2ull * p->max_stab <= 200u * 1024u) {
+      qt::Alg3ScanArgs sa{a, p->d_stables, p->d_stab_off, p->d_stab_bytes, p->max_stab};
+      QT_CUDA(qt::launch_alg3_scan(p->kind, src, sa, static_cast<uint32_t>(slices),
+                                   2ull * p->max_stab, st));
     } else {
       QT_CUDA(qt::launch_alg3(p->kind, src, a, static_cast<uint32_t>(slices), smem, st));
     }

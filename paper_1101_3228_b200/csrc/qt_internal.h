@@ -96,6 +96,15 @@ struct FinalizeArgs {
   const uint64_t* voff_col;  // [n] visits offset of layer t+1
 };
 
+// Alg III with the FP32 scan projection (d >= 2, qt_scan.cu)
+struct Alg3ScanArgs {
+  Alg3Args a;                 // a.tables: exact tables (FP64 points, global; decisions)
+  const uint8_t* stables;     // scan tables (ScanHdr + FP32 pairs), concatenated
+  const uint32_t* stab_off;   // [n]
+  const uint32_t* stab_bytes; // [n]
+  uint32_t sbuf_bytes;        // max scan table
+};
+
 // shared error text / launch counter (defined in qt_capi.cu)
 void note_error(const std::string& msg);
 void note_launches(uint64_t n);
@@ -123,6 +132,8 @@ cudaError_t launch_paths_x(int kind, bool resident, int P, const PathArgs& a, ui
 cudaError_t launch_paths_scan(int kind, int src, bool resident, int P, const ScanArgs& a,
                               uint32_t blocks, size_t smem, cudaStream_t st);
 int paths_scan_blocks_per_sm(int kind, int src, bool resident, int P, size_t smem);
+cudaError_t launch_alg3_scan(int kind, int src, const Alg3ScanArgs& a, uint32_t slices,
+                             size_t smem, cudaStream_t st);
 cudaError_t launch_nearest_scan(int dim, const uint8_t* stable, uint32_t sbytes,
                                 const uint8_t* xtable, const double* q, uint64_t nq,
                                 unsigned long long* out, cudaStream_t st);

@@ -362,6 +362,118 @@ __global__ void __launch_bounds__(scan_threads<K>(), (P >= 4 || Chain<K>::D == 3
   }
 }
 
+// Alg III (estimate.hpp:213-265) for d >= 2 with the FP32 scan projection:
+// CTA = (slice, layer k) as k_alg3, the scan tables of layers k-1 and k in
+// shared memory, P samples per thread, both projections through
+// scan_project (warp-uniform loops; dummy queries in idle slots).
+template <int K, int SRC, int P>
+__global__ void __launch_bounds__(256) k_alg3_scan(const __grid_constant__ Alg3ScanArgs f) {
+  using C = Chain<K>;
+  constexpr int D = C::D;
+  const Alg3Args& a = f.a;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t k = blockIdx.y + 1;  // transition k-1 -> k
+  const uint64_t layer0 = static_cast<uint64_t>(k - 1) * a.M;
+  uint64_t lo = layer0 + a.M * blockIdx.x / gridDim.x;
+  uint64_t hi = layer0 + a.M * (blockIdx.x + 1) / gridDim.x;
+  lo = lo > a.first ? lo : a.first;
+  hi = hi < a.first + a.count ? hi : a.first + a.count;
+  if (lo >= hi) return;
+  const uint8_t* tk = smem;
+  const uint8_t* tp = smem + f.sbuf_bytes;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    const uint32_t bytes = f.stab_bytes[k - 1] + (k >= 2 ? f.stab_bytes[k - 2] : 0u);
+    mbar_expect_tx(&bar, bytes);
+    bulk_g2s(smem, f.stables + f.stab_off[k - 1], f.stab_bytes[k - 1], &bar);
+    if (k >= 2) bulk_g2s(smem + f.sbuf_bytes, f.stables + f.stab_off[k - 2], f.stab_bytes[k - 2], &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  // layer k's exact header (global): the step and the marginal factor of layer k-1
+  const LayerTable& hx = *reinterpret_cast<const LayerTable*>(a.tables + __ldg(a.tab_off + k - 1));
+  double stp[6], mg[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    stp[c] = hx.step[c];
+    mg[c] = hx.marg_prev[c];
+  }
+  const ScanHdr& sh = *reinterpret_cast<const ScanHdr*>(tk);
+  unsigned long long* jl = a.joint + sh.joff;
+  const uint32_t npts = sh.n_pts;
+  const uint64_t len = hi - lo, T = static_cast<uint64_t>(blockDim.x) * P;
+  const uint64_t q = len / T, rem = len % T;
+  Source<SRC> src[P];
+  uint64_t cnt[P], beg[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const uint64_t v = static_cast<uint64_t>(tid) * P + p;
+    cnt[p] = q + (v < rem ? 1u : 0u);
+    beg[p] = lo + v * q + (v < rem ? v : rem);
+    if (cnt[p]) src[p].start(a.src, beg[p]);
+  }
+  const uint64_t rounds = q + (rem ? 1u : 0u);
+  for (uint64_t r = 0; r < rounds; ++r) {
+    double x[P][D], xn[P][D];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (r < cnt[p]) {
+        if (r > 0) src[p].next_unit(a.src, beg[p] + r);
+        double e[D + C::NPS];
+#pragma unroll
+        for (int q2 = 0; q2 < D + C::NPS; ++q2) e[q2] = src[p].normal();
+        C::marginal(mg, k == 1, x[p], e);  // sample_marginal(k-1, ...)
+        C::step(stp, x[p], xn[p], e + D);   // step(k-1, ...)
+      } else {
+#pragma unroll
+        for (int c = 0; c < D; ++c) x[p][c] = xn[p][c] = 0.0;
+      }
+    }
+    uint32_t j[P], i[P];
+    scan_project<D, P>(tk, a.tables, xn, j);
+    if (k >= 2) {
+      scan_project<D, P>(tp, a.tables, x, i);
+    } else {
+#pragma unroll
+      for (int p = 0; p < P; ++p) i[p] = 0;
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+      if (r < cnt[p]) red_add_u64(jl + static_cast<uint64_t>(i[p]) * npts + j[p], 1ull);
+  }
+}
+
+template <int K, int SRC>
+static cudaError_t launch_alg3_scan_t(const Alg3ScanArgs& a, dim3 g, size_t smem, cudaStream_t st) {
+  auto fn = k_alg3_scan<K, SRC, 2>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  fn<<<g, 256, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int K>
+static cudaError_t launch_alg3_scan_k(int src, const Alg3ScanArgs& a, dim3 g, size_t smem,
+                                      cudaStream_t st) {
+  switch (src) {
+    case kSrcLcg48: return launch_alg3_scan_t<K, kSrcLcg48>(a, g, smem, st);
+    case kSrcMrg: return launch_alg3_scan_t<K, kSrcMrg>(a, g, smem, st);
+    case kSrcXorwow: return launch_alg3_scan_t<K, kSrcXorwow>(a, g, smem, st);
+    default: return launch_alg3_scan_t<K, kSrcNormalsIn>(a, g, smem, st);
+  }
+}
+
+cudaError_t launch_alg3_scan(int kind, int src, const Alg3ScanArgs& a, uint32_t slices,
+                             size_t smem, cudaStream_t st) {
+  const dim3 g(slices, a.a.n);
+  return kind == 1 ? launch_alg3_scan_k<1>(src, a, g, smem, st)
+                   : launch_alg3_scan_k<3>(src, a, g, smem, st);
+}
+
 // Batch K2 (NnIndex::nearest over many queries, nn.hpp:150-167) for d >= 2:
 // the scan table staged once per CTA, P queries per thread, scan_project's
 // exact decision. Loops are warp-uniform (scan_project's rescan is

@@ -109,3 +109,29 @@ def test_scan_c5_window_vs_oracle(gpu, oracle):
     v, j = q.accumulate_paths(ch, g5, 1, 12345, 2 * 10**9, 800, 4 * 10**9)
     rv, rj = oracle.accumulate_paths(spec5, s5, p5, 1, 12345, 2 * 10**9, 800, 4 * 10**9)
     assert np.array_equal(v, rv) and np.array_equal(j, rj)
+
+
+@pytest.mark.parametrize("kind,engine", [("tf", 1), ("tf", 2), ("gbm", 1), ("gbm", 0)])
+def test_alg3_scan_equals_exact(gpu, monkeypatch, kind, engine):
+    """Alg III (layer-parallel pairs) through k_alg3_scan vs the FP64 k_alg3."""
+    import torch
+    from paper_1101_3228_b200.device import Plan
+    q = Q()
+    if kind == "tf":
+        ch = q.TwoFactorChain(q.TwoFactorParams(steps=20))
+        grids = q.build_two_factor_grids(ch, 1000)
+    else:
+        ch = q.GbmChain3d(6, 1.0, (0.2, 0.1, -0.3))
+        grids = q.build_gbm_grids(ch, 4000)
+    M = 20000
+    units = M * ch.layers()
+    out = []
+    for scan in ("1", "0"):
+        monkeypatch.setenv("QT_SCAN", scan)
+        plan = Plan(ch, grids, 0)
+        joint = plan.zeros_joint()
+        plan.count(2, engine, 4242, 0, units, units, joint)
+        torch.cuda.synchronize()
+        out.append(joint.cpu().numpy().copy())
+        plan.close()
+    assert np.array_equal(out[0], out[1])
