@@ -59,11 +59,31 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if not force and up_to_date():
             return LIB
         tmp = f"{LIB}.tmp{os.getpid()}"
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-o", tmp, *sources(), "-ldl"]
-        if verbose:
-            print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
-        os.replace(tmp, LIB)
+        # one nvcc per translation unit in parallel (no relocatable device code:
+        # every kernel lives in one TU), then one host link
+        from concurrent.futures import ThreadPoolExecutor
+        objdir = os.path.join(LIB_DIR, f".obj{os.getpid()}")
+        os.makedirs(objdir, exist_ok=True)
+        compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+        def compile_one(src: str) -> str:
+            obj = os.path.join(objdir, os.path.basename(src) + ".o")
+            cmd = [nvcc(), *ARCH, *compile_flags, "-c", "-o", obj, src]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.run(cmd, check=True)
+            return obj
+
+        try:
+            with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+                objs = list(ex.map(compile_one, sources()))
+            cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs, "-ldl"]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.run(cmd, check=True)
+            os.replace(tmp, LIB)
+        finally:
+            shutil.rmtree(objdir, ignore_errors=True)
     return LIB
 
 
