@@ -1,10 +1,13 @@
 // qt_capi.cu -- host runtime behind include/qtree_cuda.h.
 //
-// Owns: validation with the reference's error taxonomy, the per-layer grid
-// tables (sorted 1-D records + bucket index, or raw points for d >= 2), the
-// RNG jump tables, device plans, multi-GPU sharding with one NCCL all-reduce,
-// and the one-call host-buffer entry points. No CPU compute fallback exists:
-// every count is produced by the kernels in qt_kernels.cu.
+// Owns: validation with the reference's error taxonomy; the per-layer device
+// tables (sorted 1-D threshold records + bucket index, FP32 scan tables for
+// d >= 2, fast-path records); the RNG jump tables; device plans and the kernel
+// selection (k_paths_x / k_paths_scan / k_alg3_* / k_paths, opt-in fast path);
+// multi-GPU sharding with one NCCL all-reduce; the one-call host-buffer entry
+// points with pinned staging; grid construction, micro-benchmarks and the
+// batch projection. No CPU compute fallback exists: every count comes from a
+// kernel (file I/O lives in qt_io.cu).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <stdint.h>

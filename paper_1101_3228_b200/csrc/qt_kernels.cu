@@ -1,19 +1,26 @@
 // qt_kernels.cu -- the sm_100a kernels of the transition estimator.
 //
-//  k_paths   K1+K2+K3 fused: Alg I/II path kernel (estimate.hpp:88-126). One
-//            thread owns a contiguous run of paths (so its MRG32k3a state
-//            flows from path to path without jumps). A producer warp streams
-//            each layer's grid table into a ring of shared-memory stages with
-//            cp.async.bulk (full/empty mbarriers); eight consumer warps do, per
-//            transition, normals -> chain step -> exact Voronoi projection
-//            (one FP64 threshold record pair) -> one red.global.add.u64 into
-//            joint[k-1][i*N_k + j].
-//  k_alg3    K4: Alg III layer-parallel pair sampler (estimate.hpp:213-265):
-//            CTA = (layer k, slice of its M samples), tables of layers k-1 and
-//            k resident in shared memory, two projections per sample.
+//  k_paths_x   the default 1-D path kernel (Brownian / OU, MRG32k3a): Alg I/II
+//              (estimate.hpp:88-126) fused K1+K2+K3 -- MRG32k3a block substream per
+//              path, FP64 Box-Muller, chain step, exact threshold projection, one
+//              red.global.add.u64 into joint[k-1][i*N_k + j]. Lockstep CTA
+//              pipeline: thread 0 prefetches two-layer table stages with
+//              cp.async.bulk, one named barrier per two layers, P paths per thread.
+//  k_paths     the same path for every engine and for parity mode (normals in),
+//              d = 1..3: a warp-specialised TMA producer and a full/empty mbarrier
+//              ring of layer tables.
+//  k_paths_fast + k_replay  opt-in 1-D fast path: FP32 Box-Muller with verified
+//              error bounds, certified FP32 cell records, exact replay of the
+//              uncertified paths (identical counts).
+//  k_alg3_x / k_alg3  K4: Alg III layer-parallel pair sampler (estimate.hpp:213-265):
+//              CTA = (layer k, slice of its M samples), tables of layers k-1 and k
+//              resident in shared memory, two projections per sample.
 //  k_colsum / k_rowsum / k_normalize
-//            visits from the joint counts + row normalisation (quant_tree.hpp:69-83).
-//  k_nearest, k_path_normals, k_uniforms  standalone K2 and RNG probes.
+//              visits from the joint counts + row normalisation (quant_tree.hpp:69-83).
+//  k_nearest, k_path_normals, k_uniforms, k_fast_bounds_check  standalone K2, RNG
+//              probes and the exhaustive FP32 Box-Muller bound check.
+// d >= 2 path kernels live in qt_scan.cu, the pricers in qt_bdp.cu, grid
+// construction in qt_lloyd.cu, micro-benchmarks in qt_bench.cu.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
