@@ -702,6 +702,7 @@ struct qt_plan {
   uint64_t nvis = 0, njoint = 0, max_cols = 0, max_rows = 0, max_elems = 0;
   std::vector<uint32_t> tab_off, tab_bytes;
   uint32_t max_tab = 0, total_tab = 0, stages = 2;
+  bool gmem = false;  // some exact table exceeds kMaxTableBytes
   int sm_count = 148;
   uint8_t* d_tables = nullptr;
   uint32_t* d_tab_off = nullptr;
@@ -792,10 +793,7 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
                                 chain->marginal + 6 * (k - 1), p->joff[k - 1], p->sizes[k - 1],
                                 static_cast<uint32_t>(k)));
     const auto& t = blobs.back().hot;
-    if (t.size() > kMaxTableBytes)
-      raise(QT_ERR_INVALID_ARGUMENT,
-            "estimate: layer " + std::to_string(k) + " grid table (" + std::to_string(t.size()) +
-                " B) exceeds the shared-memory staging limit");
+    if (t.size() > kMaxTableBytes) p->gmem = true;  // too big to stage: global-memory kernels
     p->tab_off.push_back(static_cast<uint32_t>(p->host_tables.size()));
     p->tab_bytes.push_back(static_cast<uint32_t>(t.size()));
     p->max_tab = std::max<uint32_t>(p->max_tab, static_cast<uint32_t>(t.size()));
@@ -976,7 +974,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       return 2;
     }
     if (src == QT_ENGINE_MRG32K3A && (p->kind == QT_CHAIN_BROWNIAN_1D || p->kind == QT_CHAIN_OU_1D) &&
-        xkernel_enabled()) {  // 1-D MRG32k3a: the lockstep exact kernel
+        xkernel_enabled() && !p->gmem) {  // 1-D MRG32k3a: the lockstep exact kernel
       int P = 2;
       if (const char* e = std::getenv("QT_X_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 4 ? 4 : 2;
       qt::PathArgs xa = a;
@@ -1037,6 +1035,17 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       g_launches.fetch_add(1);
       return 1;
     }
+    if (p->gmem) {  // tables too large to stage: read them from global memory
+      uint64_t gblocks = static_cast<uint64_t>(p->sm_count) * 8;
+      const uint64_t gneed = (count + 255) / 256;
+      if (gneed < gblocks) gblocks = gneed;
+      const uint64_t T = gblocks * 256;
+      a.q = count / T;
+      a.rem = count % T;
+      QT_CUDA(qt::launch_gmem(p->kind, src, false, a, qt::Alg3Args{}, static_cast<uint32_t>(gblocks), st));
+      g_launches.fetch_add(1);
+      return 1;
+    }
     const int bps = qt::paths_blocks_per_sm(p->kind, src, resident, smem);
     uint64_t blocks = static_cast<uint64_t>(p->sm_count) * bps;
     const uint64_t need = (count + qt::kPathConsumers - 1) / qt::kPathConsumers;
@@ -1069,7 +1078,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
     slices = std::min(slices, cap);
     slices = std::min<uint64_t>(slices, 1u << 30);
     if (src == QT_ENGINE_MRG32K3A && (p->kind == QT_CHAIN_BROWNIAN_1D || p->kind == QT_CHAIN_OU_1D) &&
-        xkernel_enabled()) {
+        xkernel_enabled() && !p->gmem) {
       int P = 1;  // measured best for C3 (tools/alg3_probe.py)
       if (const char* e = std::getenv("QT_X_P")) P = std::atoi(e) == 2 ? 2 : std::atoi(e) == 4 ? 4 : 1;
       QT_CUDA(qt::launch_alg3_x(p->kind, P, a, static_cast<uint32_t>(slices), smem, st));
@@ -1077,6 +1086,10 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       qt::Alg3ScanArgs sa{a, p->d_stables, p->d_stab_off, p->d_stab_bytes, p->max_stab};
       QT_CUDA(qt::launch_alg3_scan(p->kind, src, sa, static_cast<uint32_t>(slices),
                                    2ull * p->max_stab, st));
+    } else if (p->gmem) {  // tables too large to stage: read them from global memory
+      const uint64_t gneed = (count + 255) / 256;
+      const uint64_t gblocks = std::min<uint64_t>(gneed, static_cast<uint64_t>(p->sm_count) * 8);
+      QT_CUDA(qt::launch_gmem(p->kind, src, true, qt::PathArgs{}, a, static_cast<uint32_t>(gblocks), st));
     } else {
       QT_CUDA(qt::launch_alg3(p->kind, src, a, static_cast<uint32_t>(slices), smem, st));
     }

@@ -141,6 +141,8 @@ cudaError_t launch_alg3(int kind, int src, const Alg3Args& a, uint32_t slices, s
                         cudaStream_t st);
 cudaError_t launch_alg3_x(int kind, int P, const Alg3Args& a, uint32_t slices, size_t smem,
                           cudaStream_t st);
+cudaError_t launch_gmem(int kind, int src, bool alg3, const PathArgs& pa, const Alg3Args& aa,
+                        uint32_t blocks, cudaStream_t st);
 cudaError_t launch_finalize(bool alg3, const unsigned long long* joint, unsigned long long* visits,
                             double* pi, uint64_t samples, const FinalizeArgs& f, uint32_t n,
                             uint64_t max_cols, uint64_t max_rows, uint64_t max_elems,

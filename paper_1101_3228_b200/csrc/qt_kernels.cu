@@ -769,6 +769,100 @@ __global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg
 }
 
 // ---------------------------------------------------------------------------
+// Grids whose tables exceed the shared-memory staging limit (e.g. 1-D N above
+// ~6800): the same exact arithmetic with every table read from global memory
+// through L1/L2 -- Alg I/II one path per thread slot, Alg III one sample.
+// ---------------------------------------------------------------------------
+template <int K, int SRC>
+__global__ void __launch_bounds__(256) k_paths_gmem(const __grid_constant__ PathArgs a) {
+  using C = Chain<K>;
+  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t mycount = a.q + (gid < a.rem ? 1u : 0u);
+  const uint64_t mybeg = a.first + gid * a.q + (gid < a.rem ? gid : a.rem);
+  if (!mycount) return;
+  Source<SRC> src;
+  src.start(a.src, mybeg);
+  for (uint64_t r = 0; r < mycount; ++r) {
+    if (r > 0) src.next_unit(a.src, mybeg + r);
+    double x[C::D];
+#pragma unroll
+    for (int d = 0; d < C::D; ++d) x[d] = 0.0;
+    uint32_t i = 0;
+    for (uint32_t k = 1; k <= a.n; ++k) {
+      const uint8_t* tb = a.tables + __ldg(a.tab_off + k - 1);
+      const LayerTable& h = *reinterpret_cast<const LayerTable*>(tb);
+      double e[C::NPS], xn[C::D];
+#pragma unroll
+      for (int q = 0; q < C::NPS; ++q) e[q] = src.normal();
+      C::step(h.step, x, xn, e);
+#pragma unroll
+      for (int d = 0; d < C::D; ++d) x[d] = xn[d];
+      const uint32_t j = nearest<C::D>(h, tb, x, a.tables);
+      red_add_u64(a.joint + h.joff + static_cast<uint64_t>(i) * h.n_pts + j, 1ull);
+      i = j;
+    }
+  }
+}
+
+template <int K, int SRC>
+__global__ void __launch_bounds__(256) k_alg3_gmem(const __grid_constant__ Alg3Args a) {
+  using C = Chain<K>;
+  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t q = a.count / T, rem = a.count % T;
+  const uint64_t mycount = q + (gid < rem ? 1u : 0u);
+  const uint64_t mybeg = a.first + gid * q + (gid < rem ? gid : rem);
+  if (!mycount) return;
+  Source<SRC> src;
+  src.start(a.src, mybeg);
+  for (uint64_t r = 0; r < mycount; ++r) {
+    if (r > 0) src.next_unit(a.src, mybeg + r);
+    const uint64_t unit = mybeg + r;
+    const uint32_t k = static_cast<uint32_t>(unit / a.M) + 1;  // layer-major units (k-1) M + m
+    const uint8_t* tk = a.tables + __ldg(a.tab_off + k - 1);
+    const LayerTable& hk = *reinterpret_cast<const LayerTable*>(tk);
+    double e[C::D + C::NPS], x[C::D], xn[C::D];
+#pragma unroll
+    for (int q2 = 0; q2 < C::D + C::NPS; ++q2) e[q2] = src.normal();
+    C::marginal(hk.marg_prev, k == 1, x, e);
+    C::step(hk.step, x, xn, e + C::D);
+    uint32_t i = 0;
+    if (k >= 2) {
+      const uint8_t* tp = a.tables + __ldg(a.tab_off + k - 2);
+      i = nearest<C::D>(*reinterpret_cast<const LayerTable*>(tp), tp, x, a.tables);
+    }
+    const uint32_t j = nearest<C::D>(hk, tk, xn, a.tables);
+    red_add_u64(a.joint + hk.joff + static_cast<uint64_t>(i) * hk.n_pts + j, 1ull);
+  }
+}
+
+template <int K>
+static cudaError_t launch_gmem_k(bool alg3, int src, const PathArgs& pa, const Alg3Args& aa,
+                                 uint32_t blocks, cudaStream_t st) {
+#define QT_GMEM(S)                                                           \
+  if (alg3) k_alg3_gmem<K, S><<<blocks, 256, 0, st>>>(aa);                  \
+  else k_paths_gmem<K, S><<<blocks, 256, 0, st>>>(pa);                      \
+  return cudaGetLastError();
+  switch (src) {
+    case kSrcLcg48: QT_GMEM(kSrcLcg48)
+    case kSrcMrg: QT_GMEM(kSrcMrg)
+    case kSrcXorwow: QT_GMEM(kSrcXorwow)
+    default: QT_GMEM(kSrcNormalsIn)
+  }
+#undef QT_GMEM
+}
+
+cudaError_t launch_gmem(int kind, int src, bool alg3, const PathArgs& pa, const Alg3Args& aa,
+                        uint32_t blocks, cudaStream_t st) {
+  switch (kind) {
+    case 0: return launch_gmem_k<0>(alg3, src, pa, aa, blocks, st);
+    case 1: return launch_gmem_k<1>(alg3, src, pa, aa, blocks, st);
+    case 2: return launch_gmem_k<2>(alg3, src, pa, aa, blocks, st);
+    default: return launch_gmem_k<3>(alg3, src, pa, aa, blocks, st);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // finalize
 // ---------------------------------------------------------------------------
 // visits[k][j] = sum_i joint[k-1][i][j]  (grid.y = transition t = k-1)
