@@ -230,7 +230,7 @@ struct TreeOnDevice {
     pi.alloc(poff[n]);
     phi.alloc(voff[n + 1]);
     BDP_CUDA(cudaMemcpy(visits.p, h_visits, voff[n + 1] * 8, cudaMemcpyHostToDevice));
-    BDP_CUDA(cudaMemcpy(pi.p, h_pi, poff[n] * 8, cudaMemcpyHostToDevice));
+    BDP_CUDA(qt::staged_copy(pi.p, h_pi, poff[n] * 8, true, 0));  // GBs for d >= 2 trees
     BDP_CUDA(cudaMemcpy(phi.p, h_phi, voff[n + 1] * 8, cudaMemcpyHostToDevice));
     build_csr(n, sizes, pi.p, poff, csr);
   }
@@ -285,8 +285,8 @@ QT_API qt_status qt_bdp_stopping(int32_t layers, const uint64_t* sizes, const ui
     }
     BDP_CUDA(cudaGetLastError());
     BDP_CUDA(cudaMemcpy(price, v.p, 8, cudaMemcpyDeviceToHost));
-    if (value) BDP_CUDA(cudaMemcpy(value, v.p, t.voff[n + 1] * 8, cudaMemcpyDeviceToHost));
-    if (exercise) BDP_CUDA(cudaMemcpy(exercise, ex.p, t.voff[n + 1], cudaMemcpyDeviceToHost));
+    if (value) BDP_CUDA(qt::staged_copy(value, v.p, t.voff[n + 1] * 8, false, 0));
+    if (exercise) BDP_CUDA(qt::staged_copy(exercise, ex.p, t.voff[n + 1], false, 0));
   });
 }
 
@@ -338,8 +338,8 @@ QT_API qt_status qt_bdp_swing(int32_t layers, const uint64_t* sizes, const uint6
     }
     BDP_CUDA(cudaGetLastError());
     BDP_CUDA(cudaMemcpy(price, P.p, 8, cudaMemcpyDeviceToHost));
-    if (value_all) BDP_CUDA(cudaMemcpy(value_all, P.p, soff[n + 1] * 8, cudaMemcpyDeviceToHost));
-    if (take_all && soff[n]) BDP_CUDA(cudaMemcpy(take_all, take.p, soff[n], cudaMemcpyDeviceToHost));
+    if (value_all) BDP_CUDA(qt::staged_copy(value_all, P.p, soff[n + 1] * 8, false, 0));
+    if (take_all && soff[n]) BDP_CUDA(qt::staged_copy(take_all, take.p, soff[n], false, 0));
   });
 }
 

@@ -1152,54 +1152,8 @@ double ms_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
-// Device -> pageable host copy through a pinned double buffer: the DMA of chunk
-// c+1 overlaps the (multi-threaded) memcpy of chunk c into the caller's buffer.
-// A plain cudaMemcpy into pageable memory runs at a few GB/s (staging + page
-// faults on freshly allocated output arrays); this keeps PCIe/C2C busy.
 void d2h_pinned(void* dst, const void* src, size_t bytes, cudaStream_t st) {
-  constexpr size_t kChunk = 32u << 20;
-  static std::mutex mu;
-  static uint8_t* pin[2] = {nullptr, nullptr};
-  std::lock_guard<std::mutex> lk(mu);
-  if (bytes < (4u << 20)) {  // small: direct
-    QT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
-    QT_CUDA(cudaStreamSynchronize(st));
-    return;
-  }
-  if (!pin[0]) {
-    QT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&pin[0]), kChunk, cudaHostAllocDefault));
-    QT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&pin[1]), kChunk, cudaHostAllocDefault));
-  }
-  cudaEvent_t ev[2];
-  QT_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-  QT_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
-  auto par_copy = [](uint8_t* d, const uint8_t* s, size_t n) {
-    constexpr int kT = 8;
-    std::vector<std::thread> th;
-    const size_t per = (n + kT - 1) / kT;
-    for (int t = 1; t < kT; ++t) {
-      const size_t b = per * t, e = std::min(n, b + per);
-      if (b < e) th.emplace_back([=] { std::memcpy(d + b, s + b, e - b); });
-    }
-    std::memcpy(d, s, std::min(n, per));
-    for (auto& x : th) x.join();
-  };
-  const size_t nchunks = (bytes + kChunk - 1) / kChunk;
-  auto issue = [&](size_t c) {
-    const size_t off = c * kChunk, n = std::min(kChunk, bytes - off);
-    QT_CUDA(cudaMemcpyAsync(pin[c & 1], static_cast<const uint8_t*>(src) + off, n,
-                            cudaMemcpyDeviceToHost, st));
-    QT_CUDA(cudaEventRecord(ev[c & 1], st));
-  };
-  issue(0);
-  for (size_t c = 0; c < nchunks; ++c) {
-    if (c + 1 < nchunks) issue(c + 1);
-    QT_CUDA(cudaEventSynchronize(ev[c & 1]));
-    const size_t off = c * kChunk, n = std::min(kChunk, bytes - off);
-    par_copy(static_cast<uint8_t*>(dst) + off, pin[c & 1], n);
-  }
-  cudaEventDestroy(ev[0]);
-  cudaEventDestroy(ev[1]);
+  QT_CUDA(qt::staged_copy(dst, src, bytes, false, st));
 }
 
 // Shared body of qt_estimate / qt_estimate_normals / qt_accumulate_paths.
@@ -1356,6 +1310,74 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
 namespace qt {
 void note_error(const std::string& msg) { g_error = msg; }
 void note_launches(uint64_t n) { g_launches.fetch_add(n); }
+
+// Pageable host <-> device copy through a pinned double buffer: the DMA of one
+// 32 MB chunk overlaps the (8-thread) memcpy of the next/previous chunk between
+// the caller's buffer and pinned memory. A plain cudaMemcpy on pageable memory
+// runs at a few GB/s (driver staging + page faults on fresh arrays); this keeps
+// the host link busy. The two pinned buffers are shared and serialised.
+cudaError_t staged_copy(void* dst, const void* src, size_t bytes, bool to_device,
+                        cudaStream_t st) {
+  constexpr size_t kChunk = 32u << 20;
+  static std::mutex mu;
+  static uint8_t* pin[2] = {nullptr, nullptr};
+  std::lock_guard<std::mutex> lk(mu);
+  const cudaMemcpyKind kind = to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  cudaError_t e = cudaSuccess;
+  if (bytes < (4u << 20)) {  // small: direct
+    if ((e = cudaMemcpyAsync(dst, src, bytes, kind, st)) != cudaSuccess) return e;
+    return cudaStreamSynchronize(st);
+  }
+  for (auto*& b : pin)
+    if (!b && (e = cudaHostAlloc(reinterpret_cast<void**>(&b), kChunk, cudaHostAllocDefault)))
+      return e;
+  auto par_copy = [](uint8_t* d, const uint8_t* s, size_t n) {
+    constexpr int kT = 8;
+    std::vector<std::thread> th;
+    const size_t per = (n + kT - 1) / kT;
+    for (int t = 1; t < kT; ++t) {
+      const size_t b = per * t, en = std::min(n, b + per);
+      if (b < en) th.emplace_back([=] { std::memcpy(d + b, s + b, en - b); });
+    }
+    std::memcpy(d, s, std::min(n, per));
+    for (auto& x : th) x.join();
+  };
+  cudaEvent_t ev[2];
+  if ((e = cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming))) return e;
+  if ((e = cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming))) {
+    cudaEventDestroy(ev[0]);
+    return e;
+  }
+  const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+  auto* d8 = static_cast<uint8_t*>(dst);
+  auto* s8 = static_cast<const uint8_t*>(src);
+  auto len = [&](size_t c) { return std::min(kChunk, bytes - c * kChunk); };
+  if (to_device) {
+    // chunk c: wait until buffer c&1 is free (DMA of c-2 done), fill it, DMA it
+    for (size_t c = 0; c < nchunks && !e; ++c) {
+      if (c >= 2 && (e = cudaEventSynchronize(ev[c & 1]))) break;
+      par_copy(pin[c & 1], s8 + c * kChunk, len(c));
+      if ((e = cudaMemcpyAsync(d8 + c * kChunk, pin[c & 1], len(c), kind, st))) break;
+      e = cudaEventRecord(ev[c & 1], st);
+    }
+    if (!e) e = cudaStreamSynchronize(st);
+  } else {
+    auto issue = [&](size_t c) {
+      cudaError_t r = cudaMemcpyAsync(pin[c & 1], s8 + c * kChunk, len(c), kind, st);
+      return r ? r : cudaEventRecord(ev[c & 1], st);
+    };
+    e = issue(0);
+    for (size_t c = 0; c < nchunks && !e; ++c) {
+      if (c + 1 < nchunks && (e = issue(c + 1))) break;
+      if ((e = cudaEventSynchronize(ev[c & 1]))) break;
+      par_copy(d8 + c * kChunk, pin[c & 1], len(c));
+    }
+  }
+  if (e) cudaStreamSynchronize(st);  // never leave a DMA in flight on the shared buffers
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  return e;
+}
 }  // namespace qt
 
 // ---------------------------------------------------------------------------

@@ -108,6 +108,9 @@ struct Alg3ScanArgs {
 // shared error text / launch counter (defined in qt_capi.cu)
 void note_error(const std::string& msg);
 void note_launches(uint64_t n);
+// pageable host <-> device copy staged through pinned buffers (qt_capi.cu)
+cudaError_t staged_copy(void* dst, const void* src, size_t bytes, bool to_device,
+                        cudaStream_t st);
 
 cudaError_t launch_paths(int kind, int src, bool resident, const PathArgs& a, uint32_t blocks,
                          size_t smem, cudaStream_t st);
