@@ -62,16 +62,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
         # one nvcc per translation unit in parallel (no relocatable device code:
         # every kernel lives in one TU), then one host link
         from concurrent.futures import ThreadPoolExecutor
-        objdir = os.path.join(LIB_DIR, f".obj{os.getpid()}")
+        # objects persist in lib/obj (git-ignored): a TU is recompiled only when
+        # it or any header is newer than its object
+        objdir = os.path.join(LIB_DIR, "obj")
         os.makedirs(objdir, exist_ok=True)
         compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+        hdr_t = max(os.path.getmtime(d) for d in deps() if not d.endswith(".cu"))
 
         def compile_one(src: str) -> str:
             obj = os.path.join(objdir, os.path.basename(src) + ".o")
-            cmd = [nvcc(), *ARCH, *compile_flags, "-c", "-o", obj, src]
+            if (not force and os.path.exists(obj) and
+                    os.path.getmtime(obj) >= max(hdr_t, os.path.getmtime(src))):
+                return obj
+            tmpo = f"{obj}.tmp{os.getpid()}"
+            cmd = [nvcc(), *ARCH, *compile_flags, "-c", "-o", tmpo, src]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
+            os.replace(tmpo, obj)
             return obj
 
         try:
@@ -83,7 +91,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             subprocess.run(cmd, check=True)
             os.replace(tmp, LIB)
         finally:
-            shutil.rmtree(objdir, ignore_errors=True)
+            if os.path.exists(tmp):
+                os.remove(tmp)
     return LIB
 
 

@@ -180,49 +180,31 @@ __device__ __forceinline__ void scan_project(const uint8_t* tb, const uint8_t* x
       b2[p] = hi;
     }
   }
-  // pass 2, warp-cooperative: for every (lane l, query p) with ok, the warp
-  // rescans l's candidate chunk(s), one point per lane (the same FMA order as
-  // pass 1, so the same bits), and a ballot of s <= tau gives the candidates.
+  // pass 2, per lane: each query rescans its own candidate chunk(s) with the
+  // pass-1 FFMA2 (same operands, same order, so the same bits) and counts the
+  // points with s <= tau, keeping the smallest index. Pairs are visited from a
+  // lane-rotated start so the 32 lanes' random chunks spread over the banks
+  // (chunks are 256 B apart: without the rotation every lane hits one bank group).
   uint32_t cnt[P], first[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     cnt[p] = 0;
-    first[p] = 0;
-    unsigned pend = __ballot_sync(0xffffffffu, ok[p]);
-    while (pend) {
-      const uint32_t l = __ffs(pend) - 1;
-      pend &= pend - 1;
-      float q[D];
-#pragma unroll
-      for (int c = 0; c < D; ++c) q[c] = __shfl_sync(0xffffffffu, nq[p][c], l);
-      const float t = __shfl_sync(0xffffffffu, tau[p], l);
-      const uint32_t ca = __shfl_sync(0xffffffffu, b1[p], l);
-      const uint32_t cb = __shfl_sync(0xffffffffu, b2[p], l);
-      const bool tw = __shfl_sync(0xffffffffu, two[p] ? 1u : 0u, l) != 0u;
-      uint32_t c_cnt = 0, c_first = 0;
-      for (uint32_t w = 0; w < (tw ? 2u : 1u); ++w) {
-        const uint32_t cc = w ? cb : ca;
-        const uint32_t pair = cc * kScanChunkPairs + (lane >> 1);
-        const bool odd = lane & 1u;
-        const float4 xy = XY[pair];
-        const float X = odd ? xy.y : xy.x, Y = odd ? xy.w : xy.z;
-        float sv;
-        if constexpr (D == 2) {
-          const float2 hb = B2[pair];
-          sv = __fmaf_rn(q[0], X, odd ? hb.y : hb.x);
-        } else {
-          const float4 zh = B4[pair];
-          sv = __fmaf_rn(q[2], odd ? zh.y : zh.x, odd ? zh.w : zh.z);
-          sv = __fmaf_rn(q[0], X, sv);
+    first[p] = 0xffffffffu;
+    if (!ok[p]) continue;
+    for (uint32_t w = 0; w < (two[p] ? 2u : 1u); ++w) {
+      const uint32_t base = (w ? b2[p] : b1[p]) * kScanChunkPairs;
+#pragma unroll 4
+      for (uint32_t jj = 0; jj < kScanChunkPairs; ++jj) {
+        const uint32_t pair = base + ((jj + lane) & (kScanChunkPairs - 1));
+        const float2 sc = pair_score<D>(XY, B4, B2, pair, nq[p]);
+        if (sc.x <= tau[p]) {
+          ++cnt[p];
+          first[p] = min(first[p], 2 * pair);
         }
-        sv = __fmaf_rn(q[1], Y, sv);
-        const unsigned m = __ballot_sync(0xffffffffu, sv <= t);
-        if (m && c_cnt == 0) c_first = cc * 2 * kScanChunkPairs + (__ffs(m) - 1);
-        c_cnt += __popc(m);
-      }
-      if (lane == l) {
-        cnt[p] = c_cnt;
-        first[p] = c_first;
+        if (sc.y <= tau[p]) {
+          ++cnt[p];
+          first[p] = min(first[p], 2 * pair + 1);
+        }
       }
     }
   }
