@@ -722,9 +722,17 @@ struct qt_plan {
   uint32_t max_ftab = 0, total_ftab = 0;
   std::vector<uint32_t> ftab_off_h, ftab_bytes_h;
   uint64_t amb_cap = 0, fast_paths = 0;
+  // d = 1: k_paths_x tables (threshold pairs), sorted -> original cell index per
+  // layer (indexed by voff), and the sorted-cell count scratch (njoint, lazy)
+  uint8_t* d_xtables = nullptr;
+  uint32_t* d_orig = nullptr;
+  unsigned long long* d_sjoint = nullptr;
 
   ~qt_plan() {
     cudaSetDevice(device);
+    cudaFree(d_xtables);
+    cudaFree(d_orig);
+    cudaFree(d_sjoint);
     if (d_stats) {
       unsigned long long st[3] = {0, 0, 0};
       if (cudaMemcpy(st, d_stats, sizeof st, cudaMemcpyDeviceToHost) == cudaSuccess) {
@@ -831,6 +839,28 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
     p->host_tables.insert(p->host_tables.end(), b.cold.begin(), b.cold.end());
   }
   p->stages = std::max<uint32_t>(2, std::min<uint32_t>(8, kStageBudget / std::max(p->max_tab, 1u)));
+  // d = 1: the k_paths_x copy of the hot tables, Thr[c] -> {t_c, t_c+1}, and the
+  // original index of every sorted cell (layer 0 = the singleton {x0})
+  std::vector<uint8_t> xtables;
+  std::vector<uint32_t> orig;
+  if (p->dim == 1) {
+    xtables.assign(p->host_tables.begin(), p->host_tables.begin() + p->total_tab);
+    orig.assign(p->nvis, 0);
+    for (int k = 1; k <= n; ++k) {
+      uint8_t* tb = xtables.data() + p->tab_off[k - 1];
+      const qt::LayerTable& h = *reinterpret_cast<const qt::LayerTable*>(tb);
+      const qt::Thr* T = reinterpret_cast<const qt::Thr*>(
+          p->host_tables.data() + p->tab_off[k - 1] + h.off_rec);
+      double* PT = reinterpret_cast<double*>(tb + h.off_rec);
+      const uint64_t N = p->sizes[k];
+      for (uint64_t c = 0; c < N; ++c) {
+        orig[p->voff[k] + c] = T[c].orig;
+        PT[2 * c] = T[c].t;
+        PT[2 * c + 1] = T[c + 1].t;
+      }
+      PT[2 * N] = PT[2 * N + 1] = std::numeric_limits<double>::infinity();
+    }
+  }
   // FP32 scan tables (d >= 2)
   std::vector<uint8_t> stables;
   std::vector<uint32_t> soff, sbytes;
@@ -868,6 +898,13 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
     QT_CUDA(cudaMalloc(&p->d_ftab_bytes, n * sizeof(uint32_t)));
     QT_CUDA(cudaMemcpy(p->d_ftab_off, foff.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
     QT_CUDA(cudaMemcpy(p->d_ftab_bytes, fbytes.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  }
+  if (!xtables.empty()) {
+    QT_CUDA(cudaMalloc(&p->d_xtables, xtables.size()));
+    QT_CUDA(cudaMemcpy(p->d_xtables, xtables.data(), xtables.size(), cudaMemcpyHostToDevice));
+    QT_CUDA(cudaMalloc(&p->d_orig, orig.size() * sizeof(uint32_t)));
+    QT_CUDA(cudaMemcpy(p->d_orig, orig.data(), orig.size() * sizeof(uint32_t),
+                       cudaMemcpyHostToDevice));
   }
   QT_CUDA(cudaMalloc(&p->d_tab_off, n * sizeof(uint32_t)));
   QT_CUDA(cudaMalloc(&p->d_tab_bytes, n * sizeof(uint32_t)));
@@ -974,7 +1011,11 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       return 2;
     }
     if (src == QT_ENGINE_MRG32K3A && (p->kind == QT_CHAIN_BROWNIAN_1D || p->kind == QT_CHAIN_OU_1D) &&
-        xkernel_enabled() && !p->gmem) {  // 1-D MRG32k3a: the lockstep exact kernel
+        xkernel_enabled() && !p->gmem && p->d_xtables) {  // 1-D MRG32k3a: the lockstep exact kernel
+      // counts go to the plan's sorted-cell scratch, then are permute-added into
+      // d_joint (calls on one plan are ordered by their streams: one scratch)
+      if (!p->d_sjoint) QT_CUDA(cudaMalloc(&p->d_sjoint, p->njoint * sizeof(uint64_t)));
+      QT_CUDA(cudaMemsetAsync(p->d_sjoint, 0, p->njoint * sizeof(uint64_t), st));
       int P = 2;
       if (const char* e = std::getenv("QT_X_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 4 ? 4 : 2;
       qt::PathArgs xa = a;
@@ -1006,10 +1047,15 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       const uint64_t T = xblocks * per_block;
       xa.q = count / T;
       xa.rem = count % T;
+      xa.joint = p->d_sjoint;
+      xa.xtables = p->d_xtables;
       QT_CUDA(qt::launch_paths_x(p->kind, resident, P, xa, static_cast<uint32_t>(xblocks), xsmem, st,
                                  nullptr));
-      g_launches.fetch_add(1);
-      return 1;
+      QT_CUDA(qt::launch_permute_add(p->d_sjoint, reinterpret_cast<unsigned long long*>(d_joint),
+                                     p->d_fin, p->d_orig, static_cast<uint32_t>(p->n),
+                                     p->max_elems, st));
+      g_launches.fetch_add(2);
+      return 2;
     }
     if (p->d_stables && scan_enabled()) {  // d >= 2: FP32 scan + exact FP64 decision
       // queries per thread: d = 2 keeps two CTAs per SM at P = 2; d = 3 is one

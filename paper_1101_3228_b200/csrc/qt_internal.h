@@ -37,6 +37,9 @@ struct PathArgs {
   uint32_t stages;            // shared-memory ring depth (power of 2, <= 8)
   uint32_t layers_per_stage;  // k_paths_x: layer tables per pipeline stage (1 or 2)
   uint32_t probe_nored;       // diagnostics only (QT_PROBE_NORED): skip the count REDs
+  const uint8_t* xtables;     // k_paths_x: the d = 1 tables with Thr[] replaced by
+                              // threshold pairs {t_c, t_c+1} (same offsets; counts are
+                              // in sorted-cell space, see launch_permute_add)
 };
 
 constexpr int kPathConsumers = 256;  // consumer threads per k_paths CTA
@@ -132,6 +135,13 @@ cudaError_t launch_sum_u64(const unsigned long long* v, uint64_t n, unsigned lon
                            cudaStream_t st);
 cudaError_t launch_paths_x(int kind, bool resident, int P, const PathArgs& a, uint32_t blocks,
                            size_t smem, cudaStream_t st, int* bps);
+// joint[t][orig_t[a] N_{t+1} + orig_{t+1}[b]] += sjoint[t][a N_{t+1} + b] for every
+// layer t (sorted-cell counts of k_paths_x -> the reference's original indices);
+// fin = the finalize table (rows, cols, joff, voff_row, voff_col; 5 x n), orig
+// indexed by voff.
+cudaError_t launch_permute_add(const unsigned long long* sjoint, unsigned long long* joint,
+                               const uint64_t* fin, const uint32_t* orig, uint32_t n,
+                               uint64_t max_elems, cudaStream_t st);
 cudaError_t launch_paths_scan(int kind, int src, bool resident, int P, const ScanArgs& a,
                               uint32_t blocks, size_t smem, cudaStream_t st);
 int paths_scan_blocks_per_sm(int kind, int src, bool resident, int P, size_t smem);

@@ -409,6 +409,29 @@ struct ExactPath {
   uint32_t i;   // cell at the previous layer
 };
 
+// Sorted position (not the original index) of the exact scan's answer: the
+// same (d2, original index) order as nearest_1d_scan.
+static __device__ __noinline__ uint32_t nearest_1d_scan_pos(const Rec1* R, uint32_t n, double x) {
+  uint32_t best = 0, best_orig = 0;
+  double bd = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  for (uint32_t s = 0; s < n; ++s) {
+    const Rec1 r = R[s];
+    const double d = __dsub_rn(x, r.v);
+    const double d2 = __dmul_rn(d, d);
+    if (d2 < bd || (d2 == bd && r.orig < best_orig)) {
+      bd = d2;
+      best = s;
+      best_orig = r.orig;
+    }
+  }
+  return best;
+}
+
+// One layer of P paths. The staged table is the x-table: Thr[] replaced by the
+// threshold pairs PT[c] = {t_c, t_c+1} (one 16-byte load decides the usual
+// two-step bracket), and the cell is kept as its SORTED position c; the
+// counts land in sorted-cell space (sjoint) and launch_permute_add maps them
+// to the reference's original indices once per count call.
 template <int K, int P>
 __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act)[P],
                                             const uint8_t* tb, uint32_t k,
@@ -418,7 +441,7 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
   const LayerTable& h = *reinterpret_cast<const LayerTable*>(tb);
   const double x_safe = h.x_safe, lo = h.lo, inv_w = h.inv_w, nb_d = h.nb_d;
   const uint32_t nb = h.nb, npts = h.n_pts;
-  const Thr* T = reinterpret_cast<const Thr*>(tb + h.off_rec);
+  const double2* PT = reinterpret_cast<const double2*>(tb + h.off_rec);
   const uint16_t* start = reinterpret_cast<const uint16_t*>(tb + h.off_start);
   unsigned long long* jl = joint + h.joff;
   double z[P];
@@ -448,18 +471,18 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
     const double x = ps[p].x;
     uint32_t j;
     if (safe[p]) {
-      const Thr r0 = T[c[p]], r1 = T[c[p] + 1];
-      if (x < r0.t) {
-        j = r0.orig;
-      } else if (x < r1.t) {
-        j = r1.orig;
+      const double2 r = PT[c[p]];
+      if (x < r.x) {
+        j = c[p];
+      } else if (x < r.y) {
+        j = c[p] + 1;
       } else {
         uint32_t cc = c[p] + 2;
-        while (!(x < T[cc].t)) ++cc;  // t_{N-1} = +inf stops the walk
-        j = T[cc].orig;
+        while (!(x < PT[cc].x)) ++cc;  // t_{N-1} = +inf stops the walk
+        j = cc;
       }
     } else {  // exact scan over the cold block (NaN / inf / |x| >= x_safe)
-      j = nearest_1d_scan(reinterpret_cast<const Rec1*>(gtables + h.cold_off), npts, x);
+      j = nearest_1d_scan_pos(reinterpret_cast<const Rec1*>(gtables + h.cold_off), npts, x);
     }
     if (act[p] && count) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + j, 1ull);
     ps[p].i = j;
@@ -486,7 +509,7 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_x(const __grid_constant_
     const uint32_t off = __ldg(a.tab_off + k0);
     const uint32_t bytes = __ldg(a.tab_off + k1) + __ldg(a.tab_bytes + k1) - off;
     mbar_expect_tx(&full[st], bytes);
-    bulk_g2s(smem + st * a.buf_bytes, a.tables + off, bytes, &full[st]);
+    bulk_g2s(smem + st * a.buf_bytes, a.xtables + off, bytes, &full[st]);
   };
   if (tid == 0) {
     for (uint32_t s = 0; s < S; ++s) mbar_init(&full[s], 1);
@@ -494,7 +517,7 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_x(const __grid_constant_
     if constexpr (RESIDENT) {
       mbar_expect_tx(&full[0], a.resident_bytes);
       for (uint32_t k = 0; k < a.n; ++k)
-        bulk_g2s(smem + (a.tab_off[k] - a.tab_off[0]), a.tables + a.tab_off[k], a.tab_bytes[k],
+        bulk_g2s(smem + (a.tab_off[k] - a.tab_off[0]), a.xtables + a.tab_off[k], a.tab_bytes[k],
                  &full[0]);
     } else {
       for (uint64_t g = 0; g < S && g < steps_total; ++g) issue(g);
@@ -865,6 +888,36 @@ cudaError_t launch_gmem(int kind, int src, bool alg3, const PathArgs& pa, const 
 // ---------------------------------------------------------------------------
 // finalize
 // ---------------------------------------------------------------------------
+// joint[t][orig_t[a] cols + orig_{t+1}[b]] += sjoint[t][a cols + b]  (grid.y = t):
+// k_paths_x's sorted-cell counts mapped to the reference's original indices.
+// Reads are coalesced; the writes of one row stay inside one row of joint.
+__global__ void k_permute_add(const unsigned long long* sjoint, unsigned long long* joint,
+                              const FinalizeArgs a, const uint32_t* orig) {
+  const uint32_t t = blockIdx.y;
+  const uint64_t rows = a.rows[t], cols = a.cols[t], elems = rows * cols;
+  const unsigned long long* S = sjoint + a.joff[t];
+  unsigned long long* J = joint + a.joff[t];
+  const uint32_t* orow = orig + a.voff_row[t];
+  const uint32_t* ocol = orig + a.voff_col[t];
+  for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < elems;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long v = S[e];
+    if (v == 0) continue;
+    const uint64_t r = e / cols, c = e - r * cols;
+    J[static_cast<uint64_t>(__ldg(orow + r)) * cols + __ldg(ocol + c)] += v;
+  }
+}
+
+cudaError_t launch_permute_add(const unsigned long long* sjoint, unsigned long long* joint,
+                               const uint64_t* fin, const uint32_t* orig, uint32_t n,
+                               uint64_t max_elems, cudaStream_t st) {
+  FinalizeArgs f{fin, fin + n, fin + 2 * n, fin + 3 * n, fin + 4 * n};
+  const uint64_t want = (max_elems + 255) / 256;
+  const uint32_t bx = static_cast<uint32_t>(want < 2048 ? (want ? want : 1) : 2048);
+  k_permute_add<<<dim3(bx, n), 256, 0, st>>>(sjoint, joint, f, orig);
+  return cudaGetLastError();
+}
+
 // visits[k][j] = sum_i joint[k-1][i][j]  (grid.y = transition t = k-1)
 __global__ void k_colsum(const unsigned long long* joint, unsigned long long* visits,
                          const FinalizeArgs a) {
