@@ -560,9 +560,9 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_x(const __grid_constant_
         mbar_wait_u32(full0 + 8u * s, ph);
       }
       exact_layer<K, P>(ps, act, tb, k, a.joint, a.tables, a.probe_nored == 0);
-      if (L == 2 && k + 1 <= a.n)
-        exact_layer<K, P>(ps, act, tb + __ldg(a.tab_bytes + k - 1), k + 1, a.joint, a.tables,
-                          a.probe_nored == 0);
+      if (L == 2 && k + 1 <= a.n)  // the next table follows this one (header.bytes)
+        exact_layer<K, P>(ps, act, tb + reinterpret_cast<const LayerTable*>(tb)->bytes, k + 1,
+                          a.joint, a.tables, a.probe_nored == 0);
       if constexpr (!RESIDENT) {
         named_barrier_sync(1, kFastThreads);  // every thread is done with stage s
         if (tid == 0 && g + S < steps_total) issue(g + S);
