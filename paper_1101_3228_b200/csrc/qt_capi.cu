@@ -939,7 +939,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
   if (count == 0) return 0;
   QT_CUDA(cudaSetDevice(p->device));
   const int src = source_of(engine, d_normals != nullptr);
-  const int launches_before = 0;
+  int extra = 0;  // launches besides the count kernel
   if (alg != QT_ALG_III) {
     const uint64_t normals = static_cast<uint64_t>(p->n) * p->nps;
     qt::PathArgs a{};
@@ -1124,10 +1124,20 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
     slices = std::min(slices, cap);
     slices = std::min<uint64_t>(slices, 1u << 30);
     if (src == QT_ENGINE_MRG32K3A && (p->kind == QT_CHAIN_BROWNIAN_1D || p->kind == QT_CHAIN_OU_1D) &&
-        xkernel_enabled() && !p->gmem) {
+        xkernel_enabled() && !p->gmem && p->d_xtables) {
       int P = 1;  // measured best for C3 (tools/alg3_probe.py)
       if (const char* e = std::getenv("QT_X_P")) P = std::atoi(e) == 2 ? 2 : std::atoi(e) == 4 ? 4 : 1;
+      // sorted-cell counts into the plan's scratch, then permute-added (as k_paths_x)
+      if (!p->d_sjoint) QT_CUDA(cudaMalloc(&p->d_sjoint, p->njoint * sizeof(uint64_t)));
+      QT_CUDA(cudaMemsetAsync(p->d_sjoint, 0, p->njoint * sizeof(uint64_t), st));
+      a.joint = p->d_sjoint;
+      a.xtables = p->d_xtables;
       QT_CUDA(qt::launch_alg3_x(p->kind, P, a, static_cast<uint32_t>(slices), smem, st));
+      QT_CUDA(qt::launch_permute_add(p->d_sjoint, reinterpret_cast<unsigned long long*>(d_joint),
+                                     p->d_fin, p->d_orig, static_cast<uint32_t>(p->n),
+                                     p->max_elems, st));
+      g_launches.fetch_add(1);
+      extra = 1;
     } else if (p->d_stables && scan_enabled() && 2ull * p->max_stab <= 200u * 1024u) {
       qt::Alg3ScanArgs sa{a, p->d_stables, p->d_stab_off, p->d_stab_bytes, p->max_stab};
       QT_CUDA(qt::launch_alg3_scan(p->kind, src, sa, static_cast<uint32_t>(slices),
@@ -1141,7 +1151,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
     }
   }
   g_launches.fetch_add(1);
-  return 1 + launches_before;
+  return 1 + extra;
 }
 
 int plan_finalize(qt_plan* p, int alg, uint64_t samples, const uint64_t* d_joint, uint64_t* d_visits,

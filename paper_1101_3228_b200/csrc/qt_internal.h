@@ -89,6 +89,7 @@ struct Alg3Args {
   uint32_t n;
   uint32_t buf_bytes;
   uint32_t probe_nored;   // diagnostics only (QT_PROBE_NORED): skip the count REDs
+  const uint8_t* xtables;  // k_alg3_x: threshold-pair tables (see PathArgs::xtables)
 };
 
 struct FinalizeArgs {

@@ -427,6 +427,23 @@ static __device__ __noinline__ uint32_t nearest_1d_scan_pos(const Rec1* R, uint3
   return best;
 }
 
+// The sorted cell of x on an x-table (threshold pairs PT[c] = {t_c, t_c+1}):
+// nearest_1d's rule with one 16-byte record per query.
+__device__ __forceinline__ uint32_t nearest_1d_pos(const LayerTable& h, const uint8_t* tb, double x,
+                                                   const uint8_t* gtables) {
+  if (!(fabs(x) < h.x_safe))
+    return nearest_1d_scan_pos(reinterpret_cast<const Rec1*>(gtables + h.cold_off), h.n_pts, x);
+  const double2* PT = reinterpret_cast<const double2*>(tb + h.off_rec);
+  const uint16_t* start = reinterpret_cast<const uint16_t*>(tb + h.off_start);
+  const uint32_t c = start[bucket_of(x, h.lo, h.inv_w, h.nb_d, h.nb)];  // all t_{<c} < x
+  const double2 r = PT[c];
+  if (x < r.x) return c;
+  if (x < r.y) return c + 1;
+  uint32_t cc = c + 2;
+  while (!(x < PT[cc].x)) ++cc;  // t_{N-1} = +inf stops the walk
+  return cc;
+}
+
 // One layer of P paths. The staged table is the x-table: Thr[] replaced by the
 // threshold pairs PT[c] = {t_c, t_c+1} (one 16-byte load decides the usual
 // two-step bracket), and the cell is kept as its SORTED position c; the
@@ -745,8 +762,8 @@ __global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg
     fence_mbar_init();
     const uint32_t bytes = a.tab_bytes[k - 1] + (k >= 2 ? a.tab_bytes[k - 2] : 0u);
     mbar_expect_tx(&bar, bytes);
-    bulk_g2s(smem, a.tables + a.tab_off[k - 1], a.tab_bytes[k - 1], &bar);
-    if (k >= 2) bulk_g2s(smem + a.buf_bytes, a.tables + a.tab_off[k - 2], a.tab_bytes[k - 2], &bar);
+    bulk_g2s(smem, a.xtables + a.tab_off[k - 1], a.tab_bytes[k - 1], &bar);
+    if (k >= 2) bulk_g2s(smem + a.buf_bytes, a.xtables + a.tab_off[k - 2], a.tab_bytes[k - 2], &bar);
   }
   __syncthreads();
   mbar_wait(&bar, 0);
@@ -784,8 +801,8 @@ __global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg
       double e0[1] = {z1[p]}, e1[1] = {z2[p]}, x[1], xn[1];
       C::marginal(hk.marg_prev, k == 1, x, e0);  // sample_marginal(k-1, ...)
       C::step(hk.step, x, xn, e1);               // step(k-1, ...)
-      const uint32_t i = k == 1 ? 0u : nearest_1d(hp, tp, x[0], a.tables);
-      const uint32_t j = nearest_1d(hk, tk, xn[0], a.tables);
+      const uint32_t i = k == 1 ? 0u : nearest_1d_pos(hp, tp, x[0], a.tables);
+      const uint32_t j = nearest_1d_pos(hk, tk, xn[0], a.tables);
       if (r < cnt[p] && !a.probe_nored) red_add_u64(jl + static_cast<uint64_t>(i) * npts + j, 1ull);
     }
   }

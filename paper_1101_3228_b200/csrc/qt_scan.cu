@@ -13,12 +13,12 @@
 //           s_i <= tau = m1 + 2 B + 2^-48 (|m1| + B + |q|^2);
 //   pass 2  if the third-best chunk minimum m3 > tau, only the best (and,
 //           when m2 <= tau, the second-best) chunk of 32 points can hold a
-//           minimiser: the warp rescans each lane's chunk(s) cooperatively,
-//           one point per lane, and a ballot of s <= tau gives the
-//           candidates; one candidate is the answer, several are
-//           resolved with the reference's FP64 d2 in index order (strict <,
-//           smallest index on ties). Otherwise (or for a non-finite / huge
-//           query) the exact FP64 scan of nearest_2d / nearest_3d runs.
+//           minimiser: each lane rescans its query's chunk(s) with the pass-1 FFMA2 and
+//           counts the points with s <= tau; one candidate is the answer,
+//           several are resolved with the reference's FP64 d2 in index order
+//           (strict <, smallest index on ties). Otherwise (or for a
+//           non-finite / huge query) the exact FP64 scan of nearest_2d /
+//           nearest_3d runs.
 // The cell is therefore always the reference's argmin; the FP32 scan only
 // decides which points need the FP64 arithmetic.
 #include <cuda_runtime.h>
@@ -111,20 +111,26 @@ __device__ __forceinline__ void scan_project(const uint8_t* tb, const uint8_t* x
     for (int p = 0; p < P; ++p) cm[p] = inf;
 #pragma unroll 2
     for (uint32_t j4 = 0; j4 < kScanChunkPairs; j4 += 4) {
+      const uint32_t pair0 = ch * kScanChunkPairs + j4;
       float2 sv[P][4];
+      float2 hb[4];
+      if constexpr (D == 2) {  // h of four pairs in two 16-byte loads
+        const float4 h01 = B4[pair0 / 2], h23 = B4[pair0 / 2 + 1];
+        hb[0] = make_float2(h01.x, h01.y);
+        hb[1] = make_float2(h01.z, h01.w);
+        hb[2] = make_float2(h23.x, h23.y);
+        hb[3] = make_float2(h23.z, h23.w);
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const uint32_t pair = ch * kScanChunkPairs + j4 + u;
-        const float4 xy = XY[pair];
-        float2 hb;
+        const float4 xy = XY[pair0 + u];
         float4 zh;
-        if constexpr (D == 2) hb = B2[pair];
-        else zh = B4[pair];
+        if constexpr (D == 3) zh = B4[pair0 + u];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           float2 t;
           if constexpr (D == 2) {
-            t = ffma2(nq[p][0], make_float2(xy.x, xy.y), hb);
+            t = ffma2(nq[p][0], make_float2(xy.x, xy.y), hb[u]);
           } else {
             t = ffma2(nq[p][2], make_float2(zh.x, zh.y), make_float2(zh.z, zh.w));
             t = ffma2(nq[p][0], make_float2(xy.x, xy.y), t);
@@ -180,7 +186,7 @@ __device__ __forceinline__ void scan_project(const uint8_t* tb, const uint8_t* x
       b2[p] = hi;
     }
   }
-  // pass 2, per lane: each query rescans its own candidate chunk(s) with the
+  // pass 2, per lane: each query rescans its candidate chunk(s) with the
   // pass-1 FFMA2 (same operands, same order, so the same bits) and counts the
   // points with s <= tau, keeping the smallest index. Pairs are visited from a
   // lane-rotated start so the 32 lanes' random chunks spread over the banks
