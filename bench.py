@@ -345,11 +345,12 @@ def run_ours(args, rank, world, local_rank):
     d2h = (plan.n_visits + 2 * plan.n_joint) * 8
     h2d = int(sum(g.data().nbytes for g in grids) + plan.sizes.nbytes + ch.step_coef.nbytes +
               ch.marg_coef.nbytes)
-    # one untimed call: process-level one-time costs (pinned staging buffers, module load)
+    # one untimed full-size call: process-level one-time costs (pinned staging
+    # buffers, module load, first use of the host copy threads)
     if world == 1:
-        Q.estimate(est, ch, grids, min(M, 10**6))
+        Q.estimate(est, ch, grids, M)
     else:
-        estimate_distributed(est, ch, grids, min(M, 10**6))
+        estimate_distributed(est, ch, grids, M)
     for _ in range(e2e_steps):
         torch.cuda.synchronize()
         barrier()
@@ -361,6 +362,8 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         barrier()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        if os.environ.get("QT_DEBUG"):
+            print(f"bench: e2e call {e2e_ms[-1]:.2f} ms", file=sys.stderr, flush=True)
     t_e2e = statistics.mean(e2e_ms)
     if world > 1:
         tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
