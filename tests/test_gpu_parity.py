@@ -147,6 +147,34 @@ def test_alg2_equals_alg1_and_device_sharding(gpu, golden):
         assert np.array_equal(joint.cpu().numpy().view(np.uint64), base.flat_joint)
 
 
+def test_1d_sorted_cell_counts_accumulate_over_windows(gpu):
+    """k_paths_x / k_alg3_x count in sorted-cell space into a plan scratch and
+    permute-add into the caller's joint: windowed plan.count calls must add up
+    to the one-call tree (Alg II, Brownian and OU; Alg III, OU), twice over
+    the same joint doubling it."""
+    import torch
+    from paper_1101_3228_b200.device import Plan
+    q = Q()
+    ou = q.OuChain1d(q.TwoFactorParams(sigma1=0.5, alpha1=1.0, sigma2=0.0, steps=6))
+    cases = [(1, q.BrownianChain1d(6), 20000), (1, ou, 20000), (2, ou, 3000)]
+    for alg, ch, M in cases:
+        grids = (q.build_ou_grids(ch, 40) if isinstance(ch, q.OuChain1d)
+                 else q.build_brownian_grids(ch, 40))
+        ref = q.estimate(alg, ch, grids, M)
+        units = M * 6 if alg == 2 else M
+        plan = Plan(ch, grids, 0)
+        for shards in (1, 3, 8):
+            joint = plan.zeros_joint()
+            for s in range(shards):
+                b, e = units * s // shards, units * (s + 1) // shards
+                plan.count(alg, 1, 12345, b, e - b, units, joint)
+            torch.cuda.synchronize()
+            assert np.array_equal(joint.cpu().numpy().view(np.uint64), ref.flat_joint), (alg, shards)
+        plan.count(alg, 1, 12345, 0, units, units, joint)
+        torch.cuda.synchronize()
+        assert np.array_equal(joint.cpu().numpy().view(np.uint64), 2 * ref.flat_joint)
+
+
 def test_c1_config_bit_exact(gpu, oracle, golden):
     """BASELINE config 1: 1-D BS put, n=10, N=100, M=1e6, MRG32k3a seed 12345."""
     q = Q()
