@@ -380,7 +380,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = 16.0 * kern_units / (t_kern / 1e3) / 1e9
     kernel_name = {"bm": "k_paths_x (exact 1-D path kernel: MRG32k3a + FP64 Box-Muller + step + "
                          "threshold projection + RED count)",
-                   "ou": "k_alg3 (layer-parallel pair sampler)" if est == 2 else "k_paths_x",
+                   "ou": "k_alg3_x (layer-parallel pair sampler)" if est == 2 else "k_paths_x",
                    "tf": "k_paths_scan (FP64 path + FP32 FFMA2 brute-force scan, exact decision)",
                    "gbm": "k_paths_scan (FP64 path + FP32 FFMA2 brute-force scan, exact decision)"}[kind]
     line = {
@@ -400,7 +400,9 @@ def run_ours(args, rank, world, local_rank):
                      "kernel": kernel_name,
                      "kernel_ms": t_kern, "peak_source": peak_src,
                      "algorithmic_bytes": "16 B per transition (u64 counter read-modify-write)",
-                     "binding_unit": "L2 atomic (RED) throughput + issue, see DESIGN.md section 4"},
+                     "binding_unit": ("instruction issue (FP64 Box-Muller, MRG32k3a, exact projection; "
+                                      "~60% issue-active) with the L1 data pipe (count REDs + "
+                                      "shared loads) at ~75%; see DESIGN.md section 4")},
         "e2e": {"value": transitions / (t_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e, "steps": e2e_steps},
         "gpu_launches": int(my_launches),

@@ -649,9 +649,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // No-return 64-bit atomic add (SASS RED.E.ADD.64): the count tally
-// `joint[t][i*N_k+j] += 1` (estimate.hpp:118).
+// `joint[t][i*N_k+j] += 1` (estimate.hpp:118). No "memory" clobber: nothing in
+// a path kernel reads the counts, so the compiler may move the next layer's
+// shared-memory loads above the RED (the count array is only read after the
+// kernel, by later launches).
 __device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v));
 }
 
 }  // namespace qt

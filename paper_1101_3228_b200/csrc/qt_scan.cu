@@ -109,8 +109,8 @@ __device__ __forceinline__ void scan_project(const uint8_t* tb, const uint8_t* x
     float cm[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) cm[p] = inf;
-#pragma unroll 2
-    for (uint32_t j4 = 0; j4 < kScanChunkPairs; j4 += 4) {
+#pragma unroll
+    for (uint32_t j4 = 0; j4 < kScanChunkPairs; j4 += 4) {  // whole chunk: one base address
       const uint32_t pair0 = ch * kScanChunkPairs + j4;
       float2 sv[P][4];
       float2 hb[4];

@@ -1,0 +1,28 @@
+# Round-end evidence on one B200, in parts (gpurun returns <= 64 MiB per call):
+#   PART=bench  bench lines (all configs), the reference arm, the launch list of
+#               the default bench command
+#   PART=kx     ncu --set full of k_paths_x (C2 grids, 1e9 transitions)
+#   PART=c4     ncu --set full of k_paths_scan (C4, 3.65e8 transitions)
+#   PART=c3     ncu --set full of k_alg3_x (C3, 3.65e8 samples)
+# Outputs land in gpurun_out/$TAG_*; summaries go to profiles/.
+TAG=${TAG:-r01e}
+O=gpurun_out
+mkdir -p $O
+case ${PART:-bench} in
+bench)
+  python bench.py > $O/${TAG}_bench_c2.json 2> $O/${TAG}_bench_c2.err
+  python bench.py --impl reference > $O/${TAG}_bench_ref.json 2>&1
+  for c in c1 c3 c4 c5; do python bench.py --config $c > $O/${TAG}_bench_$c.json 2> $O/${TAG}_bench_$c.err; done
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches_c2_default.csv \
+      python bench.py --no-cpu-baseline > $O/${TAG}_launches_bench.log 2>&1 ;;
+kx)
+  ncu --set full --clock-control none --import-source on -k regex:k_paths_x -c 1 -o $O/${TAG}_kx \
+      python bench.py --paths 2e7 --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 1 > $O/${TAG}_ncu_kx.log 2>&1 ;;
+c4)
+  ncu --set full --clock-control none --import-source on -k regex:k_paths_scan -c 1 -o $O/${TAG}_scan_c4 \
+      python bench.py --config c4 --paths 1e6 --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 1 > $O/${TAG}_ncu_c4.log 2>&1 ;;
+c3)
+  ncu --set full --clock-control none --import-source on -k regex:k_alg3_x -c 1 -o $O/${TAG}_alg3x_c3 \
+      python bench.py --config c3 --paths 1e6 --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 1 > $O/${TAG}_ncu_c3.log 2>&1 ;;
+esac
+ls -la $O | grep $TAG
