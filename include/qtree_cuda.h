@@ -141,7 +141,10 @@ QT_API qt_status qt_plan_layout(const qt_plan* plan, uint64_t* n_visits, uint64_
  * the layer-major sample indices (k-1)*M + m, total = n*M. d_normals is NULL
  * for the in-kernel engine, else a device array of the window's normals.
  * Asynchronous on `stream` (a cudaStream_t; NULL = default stream).
- * *launches (nullable) receives the number of kernels enqueued. */
+ * *launches (nullable) receives the number of kernels enqueued. The 1-D
+ * MRG32k3a kernels count in sorted-cell space into a scratch array owned by
+ * the plan and permute-add it into d_joint, so calls on ONE plan must be
+ * ordered (same stream, or synchronised); use one plan per concurrent stream. */
 QT_API qt_status qt_plan_count(qt_plan* plan, int32_t estimator, int32_t engine, uint64_t seed,
                                uint64_t first, uint64_t count, uint64_t total,
                                const double* d_normals, uint64_t* d_joint, void* stream,
