@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <stdint.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -727,9 +729,17 @@ struct qt_plan {
   uint8_t* d_xtables = nullptr;
   uint32_t* d_orig = nullptr;
   unsigned long long* d_sjoint = nullptr;
+  // one-call estimate buffers (joint, visits, pi), allocated on first use and
+  // kept with the (cached) plan
+  uint64_t* d_ojoint = nullptr;
+  uint64_t* d_ovis = nullptr;
+  double* d_opi = nullptr;
 
   ~qt_plan() {
     cudaSetDevice(device);
+    cudaFree(d_ojoint);
+    cudaFree(d_ovis);
+    cudaFree(d_opi);
     cudaFree(d_xtables);
     cudaFree(d_orig);
     cudaFree(d_sjoint);
@@ -923,6 +933,60 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
   QT_CUDA(cudaMemcpy(p->d_fin, fin.data(), fin.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
   device_tables(device);
   return p.release();
+}
+
+// Plans of recent one-call estimates, keyed by every input make_plan reads
+// (chain kind and coefficients, grid sizes and points, device), so a repeated qt_estimate on the same grids skips the host table
+// build and uploads. A call takes its plan out of the cache (exclusive use:
+// the sorted-cell scratch is per plan) and returns it afterwards; at most
+// kPlanCacheSize plans are kept. Leaked at exit on purpose (no CUDA calls from
+// static destructors).
+constexpr size_t kPlanCacheSize = 2;
+struct PlanCache {
+  std::mutex mu;
+  std::vector<std::pair<std::vector<uint8_t>, std::unique_ptr<qt_plan>>> items;
+};
+PlanCache& plan_cache() {
+  static PlanCache* c = new PlanCache;
+  return *c;
+}
+std::vector<uint8_t> plan_key(const qt_chain* chain, const qt_grids* grids, int device) {
+  std::vector<uint8_t> k;
+  auto put = [&](const void* p, size_t n) {
+    const uint8_t* b = static_cast<const uint8_t*>(p);
+    k.insert(k.end(), b, b + n);
+  };
+  const int32_t hdr[5] = {chain->kind, chain->layers, grids->dim, device, fast_enabled() ? 1 : 0};
+  put(hdr, sizeof hdr);
+  const size_t n = static_cast<size_t>(chain->layers);
+  put(chain->step, 6 * n * sizeof(double));
+  put(chain->marginal, 6 * n * sizeof(double));
+  put(grids->sizes, (n + 1) * sizeof(uint64_t));
+  uint64_t pts = 0;
+  for (size_t i = 1; i <= n; ++i) pts += grids->sizes[i];
+  put(grids->points, pts * static_cast<size_t>(grids->dim) * sizeof(double));
+  return k;
+}
+std::unique_ptr<qt_plan> take_plan(const std::vector<uint8_t>& key, const qt_chain* chain,
+                                   const qt_grids* grids, int device) {
+  {
+    PlanCache& c = plan_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (size_t i = 0; i < c.items.size(); ++i)
+      if (c.items[i].first == key) {
+        std::unique_ptr<qt_plan> p = std::move(c.items[i].second);
+        c.items.erase(c.items.begin() + static_cast<std::ptrdiff_t>(i));
+        return p;
+      }
+  }
+  return std::unique_ptr<qt_plan>(make_plan(chain, grids, device));
+}
+void give_plan(std::vector<uint8_t> key, std::unique_ptr<qt_plan> p) {
+  if (fast_enabled()) return;  // fast-path plans report their stats on destruction
+  PlanCache& c = plan_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.items.emplace_back(std::move(key), std::move(p));
+  while (c.items.size() > kPlanCacheSize) c.items.erase(c.items.begin());
 }
 
 int source_of(int engine, bool normals_in) {
@@ -1208,6 +1272,53 @@ double ms_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// Map the pages of host output buffers while the GPU computes: fresh arrays
+// (calloc / np.zeros) are lazily mapped, and faulting 100s of MB in during the
+// device->host copy costs more than the copy. MADV_POPULATE_WRITE (Linux 5.14)
+// maps without changing the contents; without it, one byte per page is
+// rewritten with its own value (the buffers are pure outputs of the call).
+class Prefault {
+ public:
+  void add(void* p, size_t bytes) {
+    if (p && bytes >= (1u << 20)) spans_.push_back({static_cast<char*>(p), bytes});
+  }
+  void start() {
+    size_t total = 0;
+    for (const auto& s : spans_) total += s.second;
+    if (total == 0) return;
+    const int nt = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, total >> 24)));
+    for (int t = 0; t < nt; ++t)
+      threads_.emplace_back([this, t, nt] {
+        const size_t pg = static_cast<size_t>(sysconf(_SC_PAGESIZE));
+        for (const auto& s : spans_) {
+          const uintptr_t b = reinterpret_cast<uintptr_t>(s.first);
+          const uintptr_t lo = (b + pg - 1) / pg * pg, hi = (b + s.second) / pg * pg;
+          if (hi <= lo) continue;
+          const size_t pages = (hi - lo) / pg;
+          const uintptr_t a = lo + pages * t / nt * pg, e = lo + pages * (t + 1) / nt * pg;
+          if (e <= a) continue;
+#ifndef MADV_POPULATE_WRITE
+#define MADV_POPULATE_WRITE 23
+#endif
+          if (madvise(reinterpret_cast<void*>(a), e - a, MADV_POPULATE_WRITE) == 0) continue;
+          for (uintptr_t q = a; q < e; q += pg) {
+            volatile char* c = reinterpret_cast<volatile char*>(q);
+            *c = *c;
+          }
+        }
+      });
+  }
+  void join() {
+    for (auto& t : threads_) t.join();
+    threads_.clear();
+  }
+  ~Prefault() { join(); }
+
+ private:
+  std::vector<std::pair<char*, size_t>> spans_;
+  std::vector<std::thread> threads_;
+};
+
 void d2h_pinned(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   QT_CUDA(qt::staged_copy(dst, src, bytes, false, st));
 }
@@ -1237,6 +1348,7 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
   const uint64_t total = accumulate ? win_total : units_total;
   const int G = devices;
   std::vector<std::unique_ptr<qt_plan>> plans(G);
+  std::vector<std::vector<uint8_t>> keys(G);
   std::vector<uint64_t*> dj(G, nullptr);
   std::vector<cudaStream_t> streams(G, nullptr);
   std::vector<cudaEvent_t> ev(4 * G, nullptr);
@@ -1246,28 +1358,28 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
   auto cleanup = [&] {
     for (int g = 0; g < G; ++g) {
       cudaSetDevice(g);
-      if (dj[g]) cudaFree(dj[g]);
       if (streams[g]) cudaStreamDestroy(streams[g]);
       for (int e = 0; e < 4; ++e)
         if (ev[4 * g + e]) cudaEventDestroy(ev[4 * g + e]);
     }
     cudaSetDevice(0);
     cudaFree(d_normals);
-    cudaFree(d_vis);
-    cudaFree(d_pi);
   };
   const bool dbg = std::getenv("QT_DEBUG") != nullptr;
   auto mark = [&](const char* what) {
     if (dbg) std::fprintf(stderr, "qtree: %-12s %9.2f ms\n", what, ms_since(t0));
   };
   try {
+    for (int g = 0; g < G; ++g) keys[g] = plan_key(chain, grids, g);
     for (int g = 0; g < G; ++g) {
-      plans[g].reset(make_plan(chain, grids, g));
+      plans[g] = take_plan(keys[g], chain, grids, g);
       mark("plan");
       QT_CUDA(cudaSetDevice(g));
       QT_CUDA(cudaStreamCreateWithFlags(&streams[g], cudaStreamNonBlocking));
       for (int e = 0; e < 4; ++e) QT_CUDA(cudaEventCreate(&ev[4 * g + e]));
-      QT_CUDA(cudaMalloc(&dj[g], plans[g]->njoint * sizeof(uint64_t)));
+      if (!plans[g]->d_ojoint)
+        QT_CUDA(cudaMalloc(&plans[g]->d_ojoint, plans[g]->njoint * sizeof(uint64_t)));
+      dj[g] = plans[g]->d_ojoint;
       QT_CUDA(cudaMemsetAsync(dj[g], 0, plans[g]->njoint * sizeof(uint64_t), streams[g]));
     }
     if (h_normals) {
@@ -1287,6 +1399,13 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
       QT_CUDA(cudaEventRecord(ev[4 * g], streams[g]));
       plan_count(plans[g].get(), alg, engine, seed, b, e - b, total, d_normals, dj[g], streams[g]);
       QT_CUDA(cudaEventRecord(ev[4 * g + 1], streams[g]));
+    }
+    Prefault prefault;  // host output pages, mapped while the counts run
+    if (!accumulate) {
+      prefault.add(visits, plans[0]->nvis * 8);
+      prefault.add(joint, plans[0]->njoint * 8);
+      prefault.add(pi, plans[0]->njoint * 8);
+      prefault.start();
     }
     if (G > 1) {
       const Nccl& nc = nccl();
@@ -1314,10 +1433,11 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
     }
     QT_CUDA(cudaSetDevice(0));
     qt_plan* p0 = plans[0].get();
-    QT_CUDA(cudaMalloc(&d_vis, p0->nvis * sizeof(uint64_t)));
+    if (!p0->d_ovis) QT_CUDA(cudaMalloc(&p0->d_ovis, p0->nvis * sizeof(uint64_t)));
+    if (!p0->d_opi) QT_CUDA(cudaMalloc(&p0->d_opi, p0->njoint * sizeof(double)));
+    d_vis = p0->d_ovis;
+    d_pi = p0->d_opi;
     const uint64_t M_for_visits = accumulate ? count : samples;
-    if (!accumulate) QT_CUDA(cudaMalloc(&d_pi, p0->njoint * sizeof(double)));
-    else QT_CUDA(cudaMalloc(&d_pi, p0->njoint * sizeof(double)));
     plan_finalize(p0, alg, M_for_visits, dj[0], d_vis, d_pi, streams[0]);
     QT_CUDA(cudaEventRecord(ev[3], streams[0]));
     std::vector<uint64_t> hv, hj;
@@ -1327,6 +1447,7 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
       QT_CUDA(cudaMemcpyAsync(hv.data(), d_vis, p0->nvis * 8, cudaMemcpyDeviceToHost, streams[0]));
       QT_CUDA(cudaMemcpyAsync(hj.data(), dj[0], p0->njoint * 8, cudaMemcpyDeviceToHost, streams[0]));
     } else {
+      prefault.join();
       d2h_pinned(visits, d_vis, p0->nvis * 8, streams[0]);
       d2h_pinned(joint, dj[0], p0->njoint * 8, streams[0]);
       if (pi) d2h_pinned(pi, d_pi, p0->njoint * 8, streams[0]);
@@ -1359,6 +1480,8 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
     throw;
   }
   cleanup();
+  for (int g = 0; g < G; ++g)
+    if (plans[g]) give_plan(std::move(keys[g]), std::move(plans[g]));
 }
 
 }  // namespace

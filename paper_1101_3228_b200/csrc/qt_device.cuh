@@ -230,6 +230,30 @@ __device__ __forceinline__ void box_muller(double u1, double u2, double& z1, dou
   z2 = __dmul_rn(r, s);
 }
 
+// box_muller() for P independent pairs, in three sweeps: the log-table loads of
+// every pair first, then sin/cos (independent of them), then the log
+// arithmetic, so the table latency overlaps the sin/cos work. Same operations,
+// same bits as box_muller().
+template <int P>
+__device__ __forceinline__ void box_muller_batch(const double (&u1)[P], const double (&u2)[P],
+                                                 double (&z1)[P], double (&z2)[P]) {
+  LogPrep lp[P];
+  double ang[P], sn[P], cs[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    lp[p] = qt_log_prep(u1[p] <= 0.0 ? 0x1p-64 : u1[p]);
+    ang[p] = __dmul_rn(kTwoPi, u2[p]);
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) qt_sincos_2pi(ang[p], &sn[p], &cs[p]);
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const double r = __dsqrt_rn(__dmul_rn(-2.0, qt_log_finish(lp[p])));
+    z1[p] = __dmul_rn(r, cs[p]);
+    z2[p] = __dmul_rn(r, sn[p]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // FP32 Box-Muller of the fast 1-D path (MRG32k3a only). It never decides a
 // cell by itself: it yields z~ together with a rigorous bound

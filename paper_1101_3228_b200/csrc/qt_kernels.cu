@@ -463,12 +463,17 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
   unsigned long long* jl = joint + h.joff;
   double z[P];
   if (k & 1u) {  // a fresh pair (stream.hpp:97-108): z1 now, z2 cached
+    double u1[P], u2[P], zs[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      uint32_t u1, u2;
-      mrg_step2(ps[p].st, u1, u2);
-      box_muller(mrg_to_unit(u1), mrg_to_unit(u2), z[p], ps[p].zs);
+      uint32_t a1, a2;
+      mrg_step2(ps[p].st, a1, a2);
+      u1[p] = mrg_to_unit(a1);
+      u2[p] = mrg_to_unit(a2);
     }
+    box_muller_batch<P>(u1, u2, z, zs);
+#pragma unroll
+    for (int p = 0; p < P; ++p) ps[p].zs = zs[p];
   } else {
 #pragma unroll
     for (int p = 0; p < P; ++p) z[p] = ps[p].zs;
@@ -789,13 +794,15 @@ __global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg
   unsigned long long* jl = a.joint + hk.joff;
   const uint32_t npts = hk.n_pts;
   for (uint64_t r = 0; r < rounds; ++r) {
-    double z1[P], z2[P];
+    double z1[P], z2[P], v1[P], v2[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       uint32_t u1, u2;
       mrg_step2(st[p], u1, u2);
-      box_muller(mrg_to_unit(u1), mrg_to_unit(u2), z1[p], z2[p]);
+      v1[p] = mrg_to_unit(u1);
+      v2[p] = mrg_to_unit(u2);
     }
+    box_muller_batch<P>(v1, v2, z1, z2);
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       double e0[1] = {z1[p]}, e1[1] = {z2[p]}, x[1], xn[1];

@@ -97,21 +97,32 @@ QT_HD void qt_logtab(int i, double* invc, double* lhi, double* llo) {
 // 1, so around u = 1 the reduced argument r = m - 1 is exact); r = m invc_i - 1
 // by one FMA, |r| <= 2^-8; log u = e ln2 + (-log invc_i) + log1p(r) with the
 // constants as hi + lo pairs and a degree-8 Taylor tail (< 1 ulp).
-QT_HD double qt_log_unit(double u) {
+// Split form: qt_log_prep does the reduction and the table loads, qt_log_finish
+// the arithmetic, so a caller can issue the loads of several logs (and other
+// independent work) before the first use. qt_log_unit = finish(prep(u)).
+struct LogPrep {
+  double m, invc, lhi, llo;
+  int e;
+};
+QT_HD LogPrep qt_log_prep(double u) {
   const int64_t b = qt_bits(u);
-  int e = static_cast<int>(b >> 52) - 1023;
+  LogPrep q;
+  q.e = static_cast<int>(b >> 52) - 1023;
   const int64_t mant = b & ((int64_t(1) << 52) - 1);
   int i = static_cast<int>((mant + (int64_t(1) << 44)) >> 45);
-  double m = qt_from_bits(mant | (int64_t(1023) << 52));
+  q.m = qt_from_bits(mant | (int64_t(1023) << 52));
   if (i == 128) {  // m in [2 - 2^-8, 2): use m/2 in [1 - 2^-9, 1), cell 0
     i = 0;
-    e += 1;
-    m = QT_MUL(m, 0.5);
+    q.e += 1;
+    q.m = QT_MUL(q.m, 0.5);
   }
-  double invc, lhi, llo;
-  qt_logtab(i, &invc, &lhi, &llo);
+  qt_logtab(i, &q.invc, &q.lhi, &q.llo);
+  return q;
+}
+QT_HD double qt_log_finish(const LogPrep& q) {
+  const double m = q.m, invc = q.invc, lhi = q.lhi, llo = q.llo;
   const double r = QT_FMA(m, invc, -1.0);
-  const double kd = static_cast<double>(e);
+  const double kd = static_cast<double>(q.e);
   const double t1 = QT_MUL(kd, QTK(4));               // exact (41-bit ln2 hi)
   const double hi = QT_ADD(t1, lhi);
   const double lo_a = QT_ADD(QT_SUB(t1, hi), lhi);    // Fast2Sum (|t1| >= |lhi| or t1 = 0)
@@ -128,6 +139,7 @@ QT_HD double qt_log_unit(double u) {
   const double lo = QT_ADD(QT_ADD(QT_FMA(kd, QTK(5), llo), QT_ADD(lo_a, lo_b)), tail);
   return QT_ADD(hi2, lo);
 }
+QT_HD double qt_log_unit(double u) { return qt_log_finish(qt_log_prep(u)); }
 
 QT_HD void qt_sincos_2pi(double a, double* s_out, double* c_out) {
   // fdlibm __kernel_sin / __kernel_cos coefficients (|x| <= pi/4)
