@@ -175,6 +175,28 @@ def test_1d_sorted_cell_counts_accumulate_over_windows(gpu):
         assert np.array_equal(joint.cpu().numpy().view(np.uint64), 2 * ref.flat_joint)
 
 
+def test_one_call_plan_cache_is_keyed_by_inputs(gpu, oracle):
+    """qt_estimate caches plans by every input byte: a repeat on the same grids
+    reuses it, a grid with one point moved or other coefficients must not,
+    and every result equals the oracle (the reference's restatement)."""
+    q = Q()
+    spec = ChainSpec(CHAIN_BROWNIAN1D, 5, sigma1=0.2, r=0.05)
+    ch = q.BrownianChain1d(5)
+    grids = q.build_brownian_grids(ch, 30)
+    moved = [q.QuantGrid(1, g.data().copy()) for g in grids]
+    moved[2].points[7] += 1e-9  # one bit of one point: a different grid
+    ch2 = q.BrownianChain1d(5, 2.0)  # same grids, other step coefficients
+    for chain, gr, sp in ((ch, grids, spec), (ch, grids, spec), (ch, moved, spec),
+                          (ch2, grids, ChainSpec(CHAIN_BROWNIAN1D, 5, sigma1=0.2, r=0.05,
+                                                 horizon=2.0)),
+                          (ch, grids, spec)):
+        t = q.estimate_alg2(chain, gr, 5000)
+        pts = np.concatenate([g.data() for g in gr])
+        ref = oracle.estimate(ALG_II, sp, t.sizes, pts, 5000, workers=2)
+        assert np.array_equal(t.flat_joint, ref.joint)
+        assert np.array_equal(t.flat_visits, ref.visits)
+
+
 def test_c1_config_bit_exact(gpu, oracle, golden):
     """BASELINE config 1: 1-D BS put, n=10, N=100, M=1e6, MRG32k3a seed 12345."""
     q = Q()
