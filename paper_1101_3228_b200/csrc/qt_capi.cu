@@ -983,6 +983,7 @@ std::unique_ptr<qt_plan> take_plan(const std::vector<uint8_t>& key, const qt_cha
 }
 void give_plan(std::vector<uint8_t> key, std::unique_ptr<qt_plan> p) {
   if (fast_enabled()) return;  // fast-path plans report their stats on destruction
+  if (const char* e = std::getenv("QT_PLAN_CACHE"); e && e[0] == '0') return;
   PlanCache& c = plan_cache();
   std::lock_guard<std::mutex> lk(c.mu);
   c.items.emplace_back(std::move(key), std::move(p));
