@@ -139,3 +139,33 @@ def test_fast_window_vs_oracle(gpu, oracle):
     assert np.array_equal(v, rv) and np.array_equal(j, rj)
     st = q.fast_stats()
     assert st["fast_paths"] >= 40000
+
+
+@pytest.mark.parametrize("case", ["dense", "single", "tiny_gap", "huge_spread"])
+def test_xtables_equal_thr_kernels_adversarial_grids(gpu, case, monkeypatch):
+    """k_paths_x / k_alg3_x (threshold-pair x-tables, sorted-cell counts +
+    permute-add) against k_paths / k_alg3 (Thr records, original-index counts)
+    on the adversarial grids above: identical Alg II and Alg III trees."""
+    q = Q()
+    n = 12
+    ch = q.BrownianChain1d(n)
+    rng = np.random.default_rng(11)
+    grids = []
+    for k in range(1, n + 1):
+        if case == "dense":
+            pts = rng.standard_normal(2000) * np.sqrt(k / n)
+        elif case == "single":
+            pts = np.array([0.1 * k]) if k % 2 else np.array([1.0, -1.0])
+        elif case == "tiny_gap":
+            base = rng.standard_normal(64)
+            pts = np.concatenate([base + 1e-13, base])
+        else:
+            pts = rng.standard_normal(100) * 1e6
+        grids.append(q.QuantGrid(1, pts))
+    for alg, M in ((1, 60000), (2, 8000)):
+        monkeypatch.setenv("QT_XKERNEL", "1")
+        x = q.estimate(alg, ch, grids, M)
+        monkeypatch.setenv("QT_XKERNEL", "0")
+        ref = q.estimate(alg, ch, grids, M)
+        assert np.array_equal(x.flat_joint, ref.flat_joint), (case, alg)
+        assert np.array_equal(x.flat_visits, ref.flat_visits), (case, alg)
