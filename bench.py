@@ -267,6 +267,7 @@ def run_ours(args, rank, world, local_rank):
     text, kind, n, N, M, est = CONFIGS[args.config]
     if args.paths:
         M = int(args.paths)
+        text = f"{text} [--paths override: M={M:.3g}]"
     ch, grids = make_inputs(args.config)
     plan = Plan(ch, grids, local_rank)
     units = M * n if est == 2 else M
@@ -350,7 +351,7 @@ def run_ours(args, rank, world, local_rank):
     if world == 1:
         Q.estimate(est, ch, grids, M)
     else:
-        estimate_distributed(est, ch, grids, M)
+        estimate_distributed(est, ch, grids, M, plan=plan)
     for _ in range(e2e_steps):
         torch.cuda.synchronize()
         barrier()
@@ -358,7 +359,7 @@ def run_ours(args, rank, world, local_rank):
         if world == 1:
             res = Q.estimate(est, ch, grids, M)
         else:
-            res = estimate_distributed(est, ch, grids, M)
+            res = estimate_distributed(est, ch, grids, M, plan=plan)
         torch.cuda.synchronize()
         barrier()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
