@@ -1106,7 +1106,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       int xbps = 1;
       QT_CUDA(qt::launch_paths_x(p->kind, resident, P, xa, 0, xsmem, st, &xbps));
       uint64_t xblocks = static_cast<uint64_t>(p->sm_count) * xbps;
-      const uint64_t per_block = 256ull * P;
+      const uint64_t per_block = static_cast<uint64_t>(qt::kXThreads) * P;
       const uint64_t xneed = (count + per_block - 1) / per_block;
       if (xneed < xblocks) xblocks = xneed;
       const uint64_t T = xblocks * per_block;

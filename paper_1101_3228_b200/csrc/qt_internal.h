@@ -43,6 +43,10 @@ struct PathArgs {
 };
 
 constexpr int kPathConsumers = 256;  // consumer threads per k_paths CTA
+#ifndef QT_X_THREADS
+#define QT_X_THREADS 256
+#endif
+constexpr int kXThreads = QT_X_THREADS;  // k_paths_x CTA: warps in layer lockstep
 
 // Fast 1-D path (FP32 Box-Muller with certified cells + exact replay).
 struct AmbEntry {

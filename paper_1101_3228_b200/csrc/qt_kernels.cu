@@ -515,7 +515,7 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
 // tables of layers 2q+1 and 2q+2, which share one Box-Muller pair, so the table
 // wait and the barrier are paid once per two layers.
 template <int K, bool RESIDENT, int P, int L>
-__global__ void __launch_bounds__(kFastThreads) k_paths_x(const __grid_constant__ PathArgs a) {
+__global__ void __launch_bounds__(kXThreads) k_paths_x(const __grid_constant__ PathArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   const uint32_t tid = threadIdx.x;
@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_x(const __grid_constant_
   }
   __syncthreads();
 
-  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * kFastThreads + tid;
+  const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * kXThreads + tid;
   ExactPath ps[P];
   uint64_t cnt[P];
 #pragma unroll
@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_x(const __grid_constant_
         exact_layer<K, P>(ps, act, tb + reinterpret_cast<const LayerTable*>(tb)->bytes, k + 1,
                           a.joint, a.tables, a.probe_nored == 0);
       if constexpr (!RESIDENT) {
-        named_barrier_sync(1, kFastThreads);  // every thread is done with stage s
+        named_barrier_sync(1, kXThreads);  // every thread is done with stage s
         if (tid == 0 && g + S < steps_total) issue(g + S);
         tb += a.buf_bytes;
         if (++s == S) {
@@ -607,12 +607,12 @@ static cudaError_t launch_x_t(const PathArgs& a, uint32_t blocks, size_t smem, c
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   if (bps) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, fn, kFastThreads, smem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, fn, kXThreads, smem) != cudaSuccess ||
         *bps < 1)
       *bps = 1;
     return cudaSuccess;
   }
-  fn<<<blocks, kFastThreads, smem, st>>>(a);
+  fn<<<blocks, kXThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
