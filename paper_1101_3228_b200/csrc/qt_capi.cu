@@ -1266,6 +1266,22 @@ const Nccl& nccl() {
   });
   return n;
 }
+// One communicator clique per device count, created on first use and kept
+// (ncclCommInitAll costs far more than a C2-sized all-reduce); calls that use
+// the same clique are serialised by its mutex. Never destroyed (process exit).
+struct NcclClique {
+  std::mutex mu;
+  std::vector<void*> comms;
+};
+NcclClique& nccl_clique(int G) {
+  static std::mutex m;
+  static std::vector<std::unique_ptr<NcclClique>>* cliques =
+      new std::vector<std::unique_ptr<NcclClique>>(65);
+  std::lock_guard<std::mutex> lk(m);
+  auto& c = (*cliques)[static_cast<size_t>(G)];
+  if (!c) c = std::make_unique<NcclClique>();
+  return *c;
+}
 constexpr int kNcclUint64 = 5;  // ncclUint64
 constexpr int kNcclSum = 0;     // ncclSum
 
@@ -1411,22 +1427,28 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
     if (G > 1) {
       const Nccl& nc = nccl();
       if (!nc.ok) raise(QT_ERR_DEVICE, "nccl: libnccl.so.2 not loadable for devices > 1");
-      std::vector<void*> comms(G);
-      std::vector<int> devs(G);
-      std::iota(devs.begin(), devs.end(), 0);
-      int rc = nc.init_all(comms.data(), G, devs.data());
-      if (rc) raise(QT_ERR_DEVICE, std::string("nccl: ") + (nc.err ? nc.err(rc) : "init failed"));
+      if (G > 64) raise(QT_ERR_INVALID_ARGUMENT, "estimate: at most 64 devices");
+      NcclClique& cq = nccl_clique(G);
+      std::lock_guard<std::mutex> clk(cq.mu);
+      int rc = 0;
+      if (cq.comms.empty()) {
+        std::vector<void*> comms(G);
+        std::vector<int> devs(G);
+        std::iota(devs.begin(), devs.end(), 0);
+        rc = nc.init_all(comms.data(), G, devs.data());
+        if (rc) raise(QT_ERR_DEVICE, std::string("nccl: ") + (nc.err ? nc.err(rc) : "init failed"));
+        cq.comms = comms;
+      }
       nc.group_start();
       for (int g = 0; g < G; ++g) {
         cudaSetDevice(g);
-        nc.all_reduce(dj[g], dj[g], plans[g]->njoint, kNcclUint64, kNcclSum, comms[g], streams[g]);
+        nc.all_reduce(dj[g], dj[g], plans[g]->njoint, kNcclUint64, kNcclSum, cq.comms[g], streams[g]);
       }
       rc = nc.group_end();
       for (int g = 0; g < G; ++g) {
         cudaSetDevice(g);
         cudaEventRecord(ev[4 * g + 2], streams[g]);
         cudaStreamSynchronize(streams[g]);
-        nc.destroy(comms[g]);
       }
       if (rc) raise(QT_ERR_DEVICE, std::string("nccl: ") + (nc.err ? nc.err(rc) : "all-reduce failed"));
     } else {
