@@ -90,6 +90,26 @@ typedef struct {
 QT_API qt_status qt_chain_coefficients(int32_t kind, const qt_model_params* params, double* step,
                                        double* marginal);
 
+/* Discounted obstacles phi[k][i] (the reference's NodePayoff, bdp.hpp:17,
+ * tabulated on the host in the reference's evaluation order):
+ *   BROWNIAN_1D / TWO_FACTOR: make_put_payoff / make_call_payoff /
+ *     make_swing_payoff(cfg, dim) (pipeline.hpp:120-170);
+ *   OU_1D (config 3, new): e^{-rt} (spot(p, t, x, 0) - K) with sigma2 = 0 for
+ *     SWING (put / call: the clamped forms) (two_factor.hpp:144-176);
+ *   GBM_3D or MAX_CALL (config 5, new): e^{-rt} max(max_a S_a - K, 0),
+ *     S_a = s0 exp((r - sigma_a^2/2) t + sigma_a x_a), sigma = gbm_sigma[3].
+ * t = k * (T / n). points_all = layers 0..n (layer 0 is {x0}), phi laid out
+ * like visits. InvalidArgument for unknown kinds or layers != params->steps. */
+typedef enum {
+  QT_PAYOFF_PUT = 0,
+  QT_PAYOFF_CALL = 1,
+  QT_PAYOFF_SWING = 2,
+  QT_PAYOFF_MAX_CALL = 3
+} qt_payoff_kind;
+QT_API qt_status qt_payoff_table(int32_t payoff, int32_t chain_kind, const qt_model_params* params,
+                                 const double* gbm_sigma, int32_t layers, const uint64_t* sizes,
+                                 const double* points_all, double* phi);
+
 typedef struct {
   int32_t dim;
   int32_t layers;
@@ -251,6 +271,14 @@ QT_API qt_status qt_plan_fast_stats(const qt_plan* plan, uint64_t* out);
  * max |s~ - s|, max(|c~|, |s~|)}; the fast path is valid iff out[0] <= kRadA,
  * out[1], out[2] <= kAng and out[3] <= 1 (qt_device.cuh). */
 QT_API qt_status qt_fast_bounds_check(double* out);
+
+/* Exhaustive device check of the Box-Muller log / sincos (csrc/qt_math.h, the
+ * restatement of glibc's __log_fma / __sincos_fma that rng/stream.hpp:57-62
+ * calls) over a whole engine domain on the current device: domain 0 = every
+ * MRG32k3a uniform (x + 1)/(m1 + 1), 1 = every XORWOW uniform v 2^-32.
+ * out[3] = order-independent checksums of the bits of log(u), sin(2 pi u),
+ * cos(2 pi u); tests/golden/glibc_checksums.json holds glibc's. */
+QT_API qt_status qt_math_checksum(int32_t domain, uint64_t* out);
 
 /* Thread-local text of the last failure on this thread. */
 QT_API const char* qt_last_error(void);

@@ -61,6 +61,9 @@ _SIGS = {
     "qt_fast_stats": [_u64p],
     "qt_plan_fast_stats": [C.c_void_p, _u64p],
     "qt_fast_bounds_check": [_f64p],
+    "qt_math_checksum": [C.c_int32, _u64p],
+    "qt_payoff_table": [C.c_int32, C.c_int32, C.POINTER(QtModelParams), _f64p, C.c_int32, _u64p,
+                        _f64p, _f64p],
     "qt_lloyd_build": [C.c_int32, C.c_uint64, C.c_int32, C.c_uint64, C.c_uint64, _f64p, C.c_uint64,
                        _f64p, _f64p],
     "qt_bench_pi": [C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, _u64p, _f64p,

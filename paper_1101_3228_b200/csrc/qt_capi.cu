@@ -1595,6 +1595,82 @@ QT_API qt_status qt_chain_coefficients(int32_t kind, const qt_model_params* para
   });
 }
 
+// ---- obstacles (pipeline.hpp:120-170, two_factor.hpp:144-176) ------------------
+// The reference builds std::function payoffs and the pricer evaluates them per
+// node; here the same expressions are tabulated once per tree on the host, in
+// the reference's evaluation order (no FMA contraction on x86-64 baseline), so
+// phi is bit-identical. std::max(a, b) is (a < b) ? b : a.
+namespace {
+double rmax(double a, double b) { return (a < b) ? b : a; }
+
+// model::spot (two_factor.hpp:144-152)
+double spot_of(const qt_model_params& p, double t, double x1, double x2) {
+  double c[3];
+  ou_cov(t, p.alpha1, p.alpha2, p.rho, c);
+  const double comp = p.sigma1 * p.sigma1 * c[0] + 2.0 * p.sigma1 * p.sigma2 * c[1] +
+                      p.sigma2 * p.sigma2 * c[2];
+  return p.s0 * std::exp(p.sigma1 * x1 + p.sigma2 * x2 - 0.5 * comp);
+}
+
+// one node's discounted obstacle; x has the chain's dimension
+double payoff_at(int payoff, int chain_kind, const qt_model_params& p, const double* gsig, int k,
+                 const double* x) {
+  const double dt = p.horizon / p.steps;
+  const double t = k * dt;
+  if (chain_kind == QT_CHAIN_GBM_3D || payoff == QT_PAYOFF_MAX_CALL) {
+    // config 5 (new): e^{-rt} max(max_a S_a - K, 0), S_a = s0 e^{(r - s_a^2/2) t + s_a x_a}
+    double best = -std::numeric_limits<double>::infinity();
+    for (int a = 0; a < 3; ++a) {
+      const double sa = p.s0 * std::exp((p.r - 0.5 * gsig[a] * gsig[a]) * t + gsig[a] * x[a]);
+      best = rmax(best, sa);
+    }
+    return std::exp(-p.r * t) * rmax(best - p.strike, 0.0);
+  }
+  if (chain_kind == QT_CHAIN_OU_1D) {
+    // config 3 (new): the 2-factor spot with sigma2 = 0 on the OU factor-1 state
+    qt_model_params q = p;
+    q.sigma2 = 0.0;
+    const double sp = spot_of(q, t, x[0], 0.0);
+    if (payoff == QT_PAYOFF_SWING) return std::exp(-q.r * t) * (sp - q.strike);
+    if (payoff == QT_PAYOFF_PUT) return std::exp(-q.r * t) * rmax(q.strike - sp, 0.0);
+    return std::exp(-q.r * t) * rmax(sp - q.strike, 0.0);
+  }
+  if (chain_kind == QT_CHAIN_BROWNIAN_1D) {
+    // make_*_payoff(cfg, 1): lognormal benchmark on the Brownian state
+    // (amer_payoff / amer_put_payoff two_factor.hpp:158-170, pipeline.hpp:160-164)
+    const double sp = p.s0 * std::exp((p.r - 0.5 * p.sigma1 * p.sigma1) * t + p.sigma1 * x[0]);
+    if (payoff == QT_PAYOFF_PUT) return std::exp(-p.r * t) * rmax(p.strike - sp, 0.0);
+    if (payoff == QT_PAYOFF_CALL) return std::exp(-p.r * t) * rmax(sp - p.strike, 0.0);
+    return std::exp(-p.r * t) * (sp - p.strike);
+  }
+  // make_*_payoff(cfg, 2): the 2-factor spot (pipeline.hpp:131-134,146-149,166-169)
+  const double sp = spot_of(p, t, x[0], x[1]);
+  if (payoff == QT_PAYOFF_PUT) return std::exp(-p.r * t) * rmax(p.strike - sp, 0.0);
+  if (payoff == QT_PAYOFF_CALL) return std::exp(-p.r * t) * rmax(sp - p.strike, 0.0);
+  return std::exp(-p.r * t) * (sp - p.strike);
+}
+}  // namespace
+
+QT_API qt_status qt_payoff_table(int32_t payoff, int32_t chain_kind, const qt_model_params* params,
+                                 const double* gbm_sigma, int32_t layers, const uint64_t* sizes,
+                                 const double* points_all, double* phi) {
+  return guarded([&] {
+    if (!params || !sizes || !points_all || !phi) raise(QT_ERR_INVALID_ARGUMENT, "null argument");
+    if (payoff < QT_PAYOFF_PUT || payoff > QT_PAYOFF_MAX_CALL)
+      raise(QT_ERR_INVALID_ARGUMENT, "payoff: unknown kind");
+    const int dim = chain_dim(chain_kind);
+    const bool maxcall = chain_kind == QT_CHAIN_GBM_3D || payoff == QT_PAYOFF_MAX_CALL;
+    if (maxcall && (dim != 3 || !gbm_sigma))
+      raise(QT_ERR_INVALID_ARGUMENT, "payoff: max-call needs the 3-D chain and gbm_sigma[3]");
+    if (layers < 1 || layers != params->steps)
+      raise(QT_ERR_INVALID_ARGUMENT, "payoff: layers must equal params->steps");
+    uint64_t o = 0;
+    for (int k = 0; k <= layers; ++k)
+      for (uint64_t i = 0; i < sizes[k]; ++i, ++o)
+        phi[o] = payoff_at(payoff, chain_kind, *params, gbm_sigma, k, points_all + o * dim);
+  });
+}
+
 QT_API qt_status qt_estimate(int32_t estimator, const qt_chain* chain, const qt_grids* grids,
                              uint64_t samples, int32_t engine, uint64_t seed, int32_t devices,
                              uint64_t* visits, uint64_t* joint, double* pi, double* phases_ms) {
@@ -2084,6 +2160,26 @@ QT_API qt_status qt_fast_bounds_check(double* out) {
       std::memcpy(&f, &h[i], 4);
       out[i] = f;
     }
+  });
+}
+
+QT_API qt_status qt_math_checksum(int32_t domain, uint64_t* out) {
+  return guarded([&] {
+    if (!out) raise(QT_ERR_INVALID_ARGUMENT, "null argument");
+    if (domain != 0 && domain != 1) raise(QT_ERR_INVALID_ARGUMENT, "domain must be 0 or 1");
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+      raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
+    unsigned long long* d = nullptr;
+    QT_CUDA(cudaMalloc(&d, 3 * sizeof(unsigned long long)));
+    cudaError_t e = cudaMemset(d, 0, 3 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = qt::launch_math_checksum(domain, d, nullptr);
+    unsigned long long h[3] = {0, 0, 0};
+    if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    QT_CUDA(e);
+    g_launches.fetch_add(1);
+    for (int i = 0; i < 3; ++i) out[i] = h[i];
   });
 }
 

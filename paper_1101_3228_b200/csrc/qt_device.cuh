@@ -213,10 +213,11 @@ __device__ __forceinline__ Xorwow xorwow_stream(uint64_t seed, uint64_t stream) 
 // ---------------------------------------------------------------------------
 // Box-Muller (stream.hpp:57-62): r = sqrt(-2 log u1), a = 2 pi u2,
 // (r cos a, r sin a); u1 <= 0 clamps to 2^-64. sqrt and the products are
-// correctly rounded like glibc's; log and sin/cos are the domain-specialised
-// kernels of qt_math.h (<= 1 ulp; 99.8 % / 96.9 % bit-identical to glibc,
-// tests/test_math_kernels.py) -- the one step that is not bit-identical by
-// construction (normals-in mode is exact).
+// correctly rounded like the host's; log and sincos are qt_math.h's
+// restatements of the glibc __log_fma / __sincos_fma the reference calls,
+// bit-identical on every engine's uniforms (tests/tools/check_math.cpp:
+// exhaustive over MRG32k3a and XORWOW, sampled over LCG48), so the normals --
+// and with them the counts -- are the reference's by construction.
 // ---------------------------------------------------------------------------
 constexpr double kTwoPi = 6.283185307179586;  // 2.0 * std::numbers::pi, exact doubling
 
@@ -230,25 +231,42 @@ __device__ __forceinline__ void box_muller(double u1, double u2, double& z1, dou
   z2 = __dmul_rn(r, s);
 }
 
-// box_muller() for P independent pairs, in three sweeps: the log-table loads of
-// every pair first, then sin/cos (independent of them), then the log
-// arithmetic, so the table latency overlaps the sin/cos work. Same operations,
-// same bits as box_muller().
+// box_muller() for P independent pairs, in sweeps: the log-table loads of
+// every pair first, then sincos (independent of them), then the log table
+// path. The 6 % of radii with u1 in [1 - 2^-4, 1) take glibc's separate
+// near-1 polynomial; those are evaluated afterwards in a loop that runs once
+// per near-1 pair of the lane (max over the warp, usually one pass) instead of
+// once per pair index. Same operations, same bits as box_muller().
 template <int P>
 __device__ __forceinline__ void box_muller_batch(const double (&u1)[P], const double (&u2)[P],
                                                  double (&z1)[P], double (&z2)[P]) {
   LogPrep lp[P];
-  double ang[P], sn[P], cs[P];
+  double v[P], ang[P], sn[P], cs[P], lg[P];
+  unsigned near = 0;
 #pragma unroll
   for (int p = 0; p < P; ++p) {
-    lp[p] = qt_log_prep(u1[p] <= 0.0 ? 0x1p-64 : u1[p]);
+    v[p] = u1[p] <= 0.0 ? 0x1p-64 : u1[p];
+    lp[p] = qt_log_prep(v[p]);
+    near |= qt_log_near1(v[p]) ? (1u << p) : 0u;
     ang[p] = __dmul_rn(kTwoPi, u2[p]);
   }
 #pragma unroll
   for (int p = 0; p < P; ++p) qt_sincos_2pi(ang[p], &sn[p], &cs[p]);
 #pragma unroll
+  for (int p = 0; p < P; ++p) lg[p] = qt_log_finish(lp[p]);
+  while (near) {
+    const int q = __ffs(near) - 1;
+    double x = v[0];
+#pragma unroll
+    for (int p = 1; p < P; ++p) x = q == p ? v[p] : x;
+    const double l = qt_log_near1_eval(x);
+#pragma unroll
+    for (int p = 0; p < P; ++p) lg[p] = q == p ? l : lg[p];
+    near &= near - 1;
+  }
+#pragma unroll
   for (int p = 0; p < P; ++p) {
-    const double r = __dsqrt_rn(__dmul_rn(-2.0, qt_log_finish(lp[p])));
+    const double r = __dsqrt_rn(__dmul_rn(-2.0, lg[p]));
     z1[p] = __dmul_rn(r, cs[p]);
     z2[p] = __dmul_rn(r, sn[p]);
   }

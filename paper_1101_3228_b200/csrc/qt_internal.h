@@ -127,6 +127,7 @@ cudaError_t launch_paths_fast(int kind, bool resident, int P, const FastArgs& a,
                               size_t smem, uint32_t replay_blocks, cudaStream_t st);
 int paths_fast_blocks_per_sm(int kind, bool resident, int P, size_t smem);
 cudaError_t launch_fast_bounds_check(unsigned int* out, cudaStream_t st);
+cudaError_t launch_math_checksum(int domain, unsigned long long* out, cudaStream_t st);
 cudaError_t launch_serial_normals(const SrcArgs& a, uint64_t first, uint64_t count, double* out,
                                   cudaStream_t st);
 cudaError_t launch_lloyd_update(const double* X, const unsigned long long* cell, uint64_t M,

@@ -684,6 +684,45 @@ __global__ void __launch_bounds__(256) k_fast_bounds_check(unsigned int* out) {
   }
 }
 
+// Exhaustive device check of the Box-Muller transcendentals over an engine's
+// whole uniform domain (domain 0: MRG32k3a u = (x + 1)/(m1 + 1), x < m1;
+// domain 1: XORWOW u = v 2^-32, v < 2^32): out[0..2] = sum over inputs i of
+// mix(i, bits(f(u_i))) mod 2^64 for f = log (u = 0 clamped to 2^-64), sin and
+// cos of 2 pi u. tests/tools/check_math.cpp computes the same sums from the
+// live glibc (tests/golden/glibc_checksums.json); equal sums = the device's
+// log/sincos equal glibc's on every input of the domain.
+__device__ __forceinline__ uint64_t mix_checksum(uint64_t i, double v) {
+  uint64_t z = static_cast<uint64_t>(__double_as_longlong(v)) + 0x9E3779B97F4A7C15ull * (i + 1);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void __launch_bounds__(256) k_math_checksum(int domain, unsigned long long* out) {
+  const uint64_t n = domain == 0 ? kM1 : (1ull << 32);
+  uint64_t sl = 0, ss = 0, sc = 0;
+  for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
+       g += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const double u = domain == 0 ? mrg_to_unit(static_cast<uint32_t>(g))
+                                 : __dmul_rn(static_cast<double>(g), 0x1p-32);
+    sl += mix_checksum(g, qt_log_unit(u <= 0.0 ? 0x1p-64 : u));
+    double sn, cs;
+    qt_sincos_2pi(__dmul_rn(kTwoPi, u), &sn, &cs);
+    ss += mix_checksum(g, sn);
+    sc += mix_checksum(g, cs);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sl += __shfl_xor_sync(0xffffffffu, sl, o);
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    sc += __shfl_xor_sync(0xffffffffu, sc, o);
+  }
+  if ((threadIdx.x & 31u) == 0) {
+    atomicAdd(out + 0, static_cast<unsigned long long>(sl));
+    atomicAdd(out + 1, static_cast<unsigned long long>(ss));
+    atomicAdd(out + 2, static_cast<unsigned long long>(sc));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Alg III: grid = (slices, n). Slice s of layer k covers samples
 // [M s / S, M (s+1) / S) of that layer; each thread a contiguous sub-run, so
@@ -1164,6 +1203,11 @@ int paths_fast_blocks_per_sm(int kind, bool resident, int P, size_t smem) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kFastThreads, smem) != cudaSuccess)
     return 1;
   return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_math_checksum(int domain, unsigned long long* out, cudaStream_t st) {
+  k_math_checksum<<<148 * 16, 256, 0, st>>>(domain, out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fast_bounds_check(unsigned int* out, cudaStream_t st) {

@@ -1,13 +1,23 @@
-// qt_math.h -- the Box-Muller transcendental kernels, specialised to their
-// input domains and written with explicitly rounded operations only, so the
-// host build (tests/tools/check_math.cpp, checked against glibc) and the
-// device build produce the same bits.
+// qt_math.h -- the Box-Muller transcendentals, bit-identical to the glibc the
+// reference calls.
 //
-//   qt_sincos_2pi(a): sin and cos of the Box-Muller angle a = 2 pi u2 in
-//   [0, 2 pi]. Cody-Waite reduction by q pi/2 with pi/2 = HI + MID + LO
-//   (HI has 3 trailing zero bits, so q HI is exact for q <= 4 and a - q HI is
-//   exact by Sterbenz), then the fdlibm-form kernels on |r| <= pi/4 with the
-//   reduction tail folded in (< 1 ulp). No table loads, no large-argument path.
+// The reference's box_muller (rng/stream.hpp:57-62) computes
+//   r = std::sqrt(-2.0 * std::log(u1)),  a = 2 pi u2,  (r cos a, r sin a)
+// and g++ -O3 turns the cos/sin pair into ONE sincos() call (objdump of the
+// reference build: `call log@plt`, `call sincos@plt`). On x86-64 hosts with
+// AVX2 + FMA (this image's CPUs) glibc 2.39 resolves those to __log_fma and
+// __sincos_fma: glibc's own C sources (sysdeps/ieee754/dbl-64/e_log.c,
+// s_sincos.c with the do_sin/do_cos/reduce_sincos of s_sin.c) compiled with
+// -mfma, where GCC fused many `a*b + c` into FMAs. This file restates those
+// two functions operation for operation -- the order of every add and which
+// products are fused were read off the disassembly of that libm build -- with
+// explicitly rounded operations only, so the host build (checked against the
+// live libm by tests/tools/check_math.cpp over ALL 2^32 - 209 MRG32k3a
+// uniforms) and the device build produce the same bits. Data tables and
+// constants: qt_glibc_tab.h (generated from that libm by tools/gen_glibc_tab.c).
+//
+//   qt_log_unit(x)      == glibc log(x)     for positive normal x (x <= 1 here)
+//   qt_sincos_2pi(x,..) == glibc sincos(x)  for |x| < 105414350 (2 pi u2 here)
 #pragma once
 
 #if defined(__CUDA_ARCH__)
@@ -16,7 +26,6 @@
 #define QT_MUL(a, b) __dmul_rn((a), (b))
 #define QT_ADD(a, b) __dadd_rn((a), (b))
 #define QT_SUB(a, b) __dsub_rn((a), (b))
-#define QT_RINT(a) rint(a)
 #else
 #include <cmath>
 #if defined(__CUDACC__)
@@ -28,147 +37,228 @@
 #define QT_MUL(a, b) ((a) * (b))
 #define QT_ADD(a, b) ((a) + (b))
 #define QT_SUB(a, b) ((a) - (b))
-#define QT_RINT(a) std::nearbyint(a)
 #endif
 
 #include <stdint.h>
 #include <string.h>
 
-#include "qt_logtab.h"
+#include "qt_glibc_tab.h"
 
 namespace qt {
 
-// The FP64 constants of both kernels. On the device they live in the constant
-// bank, so every DFMA takes them as a c[][] operand instead of rebuilding each
-// 64-bit literal with two uniform moves per use (ncu: UMOV was 12 % of the
-// path kernel's instructions); the host build reads the same values.
-#define QT_MATH_K_LIST                                                                  \
-  /* 0 */ 0x1.2492492492492p-3, -0x1.5555555555555p-3, 0x1.999999999999ap-3,          \
-  /* 3 */ 0x1.5555555555555p-2, kLn2Hi, kLn2Lo,                                        \
-  /* 6 */ -1.66666666666666324348e-01, 8.33333333332248946124e-03,                     \
-  /* 8 */ -1.98412698298579493134e-04, 2.75573137070700676789e-06,                     \
-  /* 10 */ -2.50507602534068634195e-08, 1.58969099521155010221e-10,                    \
-  /* 12 */ 4.16666666666666019037e-02, -1.38888888888741095749e-03,                    \
-  /* 14 */ 2.48015872894767294178e-05, -2.75573143513906633035e-07,                    \
-  /* 16 */ 2.08757232129817482790e-09, -1.13596475577881948265e-11,                    \
-  /* 18 */ 0x1.45f306dc9c883p-1, 0x1.921fb54442d18p+0, 0x1.1a62633145c07p-54,          \
-  /* 21 */ -0x1.f1976b7ed8fbcp-110, -0.125, -0.25, -0.5, 0.5, 1.0
 #if defined(__CUDACC__)
-static __device__ const LogEntry kLogTabDev[128] = {QT_LOGTAB_ENTRIES};
-static __constant__ double kMathKDev[] = {QT_MATH_K_LIST};
+static __device__ const double2 kGlibcLogTabDev[128] = {QT_GLIBC_LOG_TAB};
+// row i = {sn, ssn} at [2i], {cs, ccs} at [2i + 1]
+static __device__ const double2 kGlibcSincosTabDev[220] = {QT_GLIBC_SINCOS_TAB};
 #endif
-static const double kMathKHost[] = {QT_MATH_K_LIST};
+struct GlibcLogEnt {
+  double invc, logc;
+};
+static const GlibcLogEnt kGlibcLogTabHost[128] = {QT_GLIBC_LOG_TAB};
+static const double kGlibcSincosTabHost[440] = {QT_GLIBC_SINCOS_TAB};
+
 #if defined(__CUDA_ARCH__)
-#define QTK(i) (kMathKDev[i])
-#else
-#define QTK(i) (kMathKHost[i])
-#endif
-#if defined(__CUDA_ARCH__)
-QT_HD int64_t qt_bits(double x) { return __double_as_longlong(x); }
-QT_HD double qt_from_bits(int64_t b) { return __longlong_as_double(b); }
-QT_HD void qt_logtab(int i, double* invc, double* lhi, double* llo) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(&kLogTabDev[i]));
-  *invc = a.x;
-  *lhi = a.y;
-  *llo = __ldg(&kLogTabDev[i].llo);
+QT_HD uint64_t qt_bits(double x) { return static_cast<uint64_t>(__double_as_longlong(x)); }
+QT_HD double qt_from_bits(uint64_t b) { return __longlong_as_double(static_cast<long long>(b)); }
+QT_HD void glibc_log_tab(int i, double* invc, double* logc) {
+  const double2 e = __ldg(&kGlibcLogTabDev[i]);
+  *invc = e.x;
+  *logc = e.y;
 }
+QT_HD void glibc_sincos_tab(int i, double* sn, double* ssn, double* cs, double* ccs) {
+  const double2 e0 = __ldg(&kGlibcSincosTabDev[2 * i]);
+  const double2 e1 = __ldg(&kGlibcSincosTabDev[2 * i + 1]);
+  *sn = e0.x;
+  *ssn = e0.y;
+  *cs = e1.x;
+  *ccs = e1.y;
+}
+QT_HD double qt_copysign(double x, double s) { return copysign(x, s); }
+QT_HD double qt_fabs(double x) { return fabs(x); }
 #else
-static const LogEntry kLogTabHost[128] = {QT_LOGTAB_ENTRIES};
-QT_HD int64_t qt_bits(double x) {
-  int64_t b;
+QT_HD uint64_t qt_bits(double x) {
+  uint64_t b;
   memcpy(&b, &x, 8);
   return b;
 }
-QT_HD double qt_from_bits(int64_t b) {
+QT_HD double qt_from_bits(uint64_t b) {
   double x;
   memcpy(&x, &b, 8);
   return x;
 }
-QT_HD void qt_logtab(int i, double* invc, double* lhi, double* llo) {
-  *invc = kLogTabHost[i].invc;
-  *lhi = kLogTabHost[i].lhi;
-  *llo = kLogTabHost[i].llo;
+QT_HD void glibc_log_tab(int i, double* invc, double* logc) {
+  *invc = kGlibcLogTabHost[i].invc;
+  *logc = kGlibcLogTabHost[i].logc;
 }
+QT_HD void glibc_sincos_tab(int i, double* sn, double* ssn, double* cs, double* ccs) {
+  *sn = kGlibcSincosTabHost[4 * i];
+  *ssn = kGlibcSincosTabHost[4 * i + 1];
+  *cs = kGlibcSincosTabHost[4 * i + 2];
+  *ccs = kGlibcSincosTabHost[4 * i + 3];
+}
+QT_HD double qt_copysign(double x, double s) { return std::copysign(x, s); }
+QT_HD double qt_fabs(double x) { return std::fabs(x); }
 #endif
 
-// log(u) for a positive normal u <= 1 (the Box-Muller radius argument:
-// MRG32k3a gives u in [2^-32, 1), LCG48/XORWOW clamp 0 to 2^-64). u = 2^e m,
-// m in [1, 2); cell i = round(128 (m - 1)) (the top cell folds to m/2 next to
-// 1, so around u = 1 the reduced argument r = m - 1 is exact); r = m invc_i - 1
-// by one FMA, |r| <= 2^-8; log u = e ln2 + (-log invc_i) + log1p(r) with the
-// constants as hi + lo pairs and a degree-8 Taylor tail (< 1 ulp).
-// Split form: qt_log_prep does the reduction and the table loads, qt_log_finish
-// the arithmetic, so a caller can issue the loads of several logs (and other
-// independent work) before the first use. qt_log_unit = finish(prep(u)).
+// ---------------------------------------------------------------------------
+// log (e_log.c, __FP_FAST_FMA build). Inputs here are positive normals; the
+// subnormal / zero / negative / inf / NaN path of glibc is not restated.
+// ---------------------------------------------------------------------------
+constexpr uint64_t kLogLo = 0x3FEE000000000000ull;      // asuint64(1.0 - 0x1p-4)
+constexpr uint64_t kLogHiMinusLo = 0x0003090000000000ull;  // asuint64(1.0 + 0x1.09p-4) - LO
+constexpr uint64_t kLogOff = 0x3fe6000000000000ull;
+
+QT_HD bool qt_log_near1(double x) { return qt_bits(x) - kLogLo < kLogHiMinusLo; }
+
+// x in [1 - 2^-4, 1 + 0x1.09p-4): log1p(r), r = x - 1, by the degree-11
+// polynomial plus the exact-ish head r - r^2/2 (e_log.c "close to 1.0").
+QT_HD double qt_log_near1_eval(double x) {
+  using namespace glibc;
+  if (qt_bits(x) == 0x3ff0000000000000ull) return 0.0;
+  const double r = QT_SUB(x, 1.0);
+  const double r2 = QT_MUL(r, r);
+  const double r3 = QT_MUL(r, r2);
+  double t7 = QT_FMA(r, kB8, kB7);
+  t7 = QT_FMA(r2, kB9, t7);
+  t7 = QT_FMA(r3, kB10, t7);
+  double t4 = QT_FMA(r, kB5, kB4);
+  t4 = QT_FMA(r2, kB6, t4);
+  t4 = QT_FMA(t7, r3, t4);
+  double t1 = QT_FMA(r, kB2, kB1);
+  t1 = QT_FMA(r2, kB3, t1);
+  const double p = QT_FMA(t4, r3, t1);
+  const double rhi = QT_FMA(-r, 0x1p27, QT_FMA(r, 0x1p27, r));  // (r + w) - w, w = r 2^27
+  const double rlo = QT_SUB(r, rhi);
+  const double rh2 = QT_MUL(rhi, rhi);
+  const double hi = QT_FMA(rh2, kB0, r);
+  double lo = QT_FMA(rh2, kB0, QT_SUB(r, hi));
+  lo = QT_FMA(QT_MUL(kB0, rlo), QT_ADD(r, rhi), lo);
+  return QT_ADD(hi, QT_FMA(p, r3, lo));
+}
+
+// Table path, split so a caller can issue the table loads of several logs
+// before the arithmetic of the first: x = 2^k z, z in [OFF, 2 OFF),
+// r = z invc_i - 1 by one FMA, log x = k ln2 + logc_i + log1p(r).
 struct LogPrep {
-  double m, invc, lhi, llo;
-  int e;
+  double z, invc, logc, kd;
 };
-QT_HD LogPrep qt_log_prep(double u) {
-  const int64_t b = qt_bits(u);
+QT_HD LogPrep qt_log_prep(double x) {
+  const uint64_t ix = qt_bits(x);
+  const uint64_t tmp = ix - kLogOff;
+  const int i = static_cast<int>((tmp >> 45) & 127u);
+  const int k = static_cast<int>(static_cast<int64_t>(tmp) >> 52);
   LogPrep q;
-  q.e = static_cast<int>(b >> 52) - 1023;
-  const int64_t mant = b & ((int64_t(1) << 52) - 1);
-  int i = static_cast<int>((mant + (int64_t(1) << 44)) >> 45);
-  q.m = qt_from_bits(mant | (int64_t(1023) << 52));
-  if (i == 128) {  // m in [2 - 2^-8, 2): use m/2 in [1 - 2^-9, 1), cell 0
-    i = 0;
-    q.e += 1;
-    q.m = QT_MUL(q.m, 0.5);
-  }
-  qt_logtab(i, &q.invc, &q.lhi, &q.llo);
+  q.z = qt_from_bits(ix - (tmp & (0xfffull << 52)));
+  q.kd = static_cast<double>(k);
+  glibc_log_tab(i, &q.invc, &q.logc);
   return q;
 }
 QT_HD double qt_log_finish(const LogPrep& q) {
-  const double m = q.m, invc = q.invc, lhi = q.lhi, llo = q.llo;
-  const double r = QT_FMA(m, invc, -1.0);
-  const double kd = static_cast<double>(q.e);
-  const double t1 = QT_MUL(kd, QTK(4));               // exact (41-bit ln2 hi)
-  const double hi = QT_ADD(t1, lhi);
-  const double lo_a = QT_ADD(QT_SUB(t1, hi), lhi);    // Fast2Sum (|t1| >= |lhi| or t1 = 0)
-  const double hi2 = QT_ADD(hi, r);
-  const double lo_b = QT_ADD(QT_SUB(hi, hi2), r);     // Fast2Sum (|hi| >= |r| or hi = 0)
-  // log1p(r) - r = r^2 (-1/2 + r (1/3 + r (-1/4 + r (1/5 + r (-1/6 + r (1/7 - r/8))))))
-  const double p7 = QT_FMA(r, QTK(22), QTK(0));
-  const double p6 = QT_FMA(r, p7, QTK(1));
-  const double p5 = QT_FMA(r, p6, QTK(2));
-  const double p4 = QT_FMA(r, p5, -0.25);
-  const double p3 = QT_FMA(r, p4, QTK(3));
-  const double p2 = QT_FMA(r, p3, -0.5);
-  const double tail = QT_MUL(QT_MUL(r, r), p2);
-  const double lo = QT_ADD(QT_ADD(QT_FMA(kd, QTK(5), llo), QT_ADD(lo_a, lo_b)), tail);
-  return QT_ADD(hi2, lo);
+  using namespace glibc;
+  const double r = QT_FMA(q.z, q.invc, -1.0);
+  const double w = QT_FMA(q.kd, kLn2Hi, q.logc);
+  const double hi = QT_ADD(w, r);
+  const double lo = QT_FMA(q.kd, kLn2Lo, QT_ADD(QT_SUB(w, hi), r));
+  const double r2 = QT_MUL(r, r);
+  const double p = QT_FMA(r2, QT_FMA(r, kA4, kA3), QT_FMA(r, kA2, kA1));
+  const double y = QT_FMA(QT_MUL(r, r2), p, QT_FMA(r2, kA0, lo));
+  return QT_ADD(y, hi);
 }
-QT_HD double qt_log_unit(double u) { return qt_log_finish(qt_log_prep(u)); }
+QT_HD double qt_log_unit(double x) {
+  return qt_log_near1(x) ? qt_log_near1_eval(x) : qt_log_finish(qt_log_prep(x));
+}
 
-QT_HD void qt_sincos_2pi(double a, double* s_out, double* c_out) {
-  // fdlibm __kernel_sin / __kernel_cos coefficients (|x| <= pi/4)
-  const double S1 = QTK(6), S2 = QTK(7), S3 = QTK(8), S4 = QTK(9), S5 = QTK(10), S6 = QTK(11);
-  const double C1 = QTK(12), C2 = QTK(13), C3 = QTK(14), C4 = QTK(15), C5 = QTK(16),
-               C6 = QTK(17);
-  const double q = QT_RINT(QT_MUL(a, QTK(18)));  // round(a * 2/pi)
-  const double t = QT_FMA(-q, QTK(19), a);       // exact
-  const double r = QT_FMA(-q, QTK(20), t);
-  // tail: (t - r) - q MID - q LO
-  const double y = QT_FMA(-q, QTK(21), QT_FMA(-q, QTK(20), QT_SUB(t, r)));
-  const double z = QT_MUL(r, r);
-  const double v = QT_MUL(z, r);
-  // sin(r + y) = r - ((z (y/2 - v P) - y) - v S1)
-  const double ps = QT_FMA(z, QT_FMA(z, QT_FMA(z, QT_FMA(z, S6, S5), S4), S3), S2);
-  const double sn =
-      QT_SUB(r, QT_SUB(QT_SUB(QT_MUL(z, QT_FMA(-v, ps, QT_MUL(0.5, y))), y), QT_MUL(v, S1)));
-  // cos(r + y) = w + (((1 - w) - z/2) + (z Q - r y)), w = 1 - z/2
-  const double pc =
-      QT_MUL(z, QT_FMA(z, QT_FMA(z, QT_FMA(z, QT_FMA(z, QT_FMA(z, C6, C5), C4), C3), C2), C1));
-  const double hz = QT_MUL(0.5, z);
-  const double w = QT_SUB(1.0, hz);
-  const double cs =
-      QT_ADD(w, QT_ADD(QT_SUB(QT_SUB(1.0, w), hz), QT_FMA(z, pc, -QT_MUL(r, y))));
-  const int quad = static_cast<int>(q) & 3;
-  const double s1 = (quad & 1) ? cs : sn;
-  const double c1 = (quad & 1) ? sn : cs;
-  *s_out = (quad & 2) ? -s1 : s1;
-  *c_out = ((quad + 1) & 2) ? -c1 : c1;
+// ---------------------------------------------------------------------------
+// sincos (s_sincos.c with s_sin.c's do_sin / do_cos / reduce_sincos):
+//   |x| < 2^-27          sin = x, cos = 1
+//   |x| < 0.85546875     sin = do_sin(x, 0),              cos = do_cos(x, 0)
+//   |x| < 2.426265       a + da = pi/2 - |x|:  sin = copysign(do_cos(a, da), x),
+//                                              cos = do_sin(a, da)
+//   |x| < 105414350      a + da = x - n pi/2:  sin = do_sincos(a, da, n),
+//                                              cos = do_sincos(a, da, n + 1)
+// Every range evaluates one do_sin and one do_cos of the same (a, da), so the
+// restatement computes the range's (a, da, n) branch-free, then both kernels
+// (sharing their table row), then routes and signs the two results.
+// ---------------------------------------------------------------------------
+struct SincosArg {
+  double a, da;
+  int route;  // 0: (sin, cos) = (S, C); 1: (C, S); bit 2: negate sin; bit 3: negate cos
+  bool tiny;
+};
+QT_HD SincosArg qt_sincos_arg(double x) {
+  using namespace glibc;
+  const uint32_t k = static_cast<uint32_t>(qt_bits(x) >> 32) & 0x7fffffffu;
+  SincosArg g;
+  g.tiny = k < 0x3e400000u;
+  if (k < 0x3feb6000u) {
+    g.a = x;
+    g.da = 0.0;
+    g.route = 0;
+  } else if (k < 0x400368fdu) {
+    const double y = QT_SUB(kHp0, qt_fabs(x));
+    g.a = QT_ADD(y, kHp1);
+    g.da = QT_ADD(QT_SUB(y, g.a), kHp1);
+    g.route = 1 | 16;  // bit 4: sin takes the sign of x
+  } else {
+    const double t = QT_FMA(x, kHpinv, kToint);
+    const double xn = QT_SUB(t, kToint);
+    const int n = static_cast<int>(qt_bits(t) & 3u);
+    const double y = QT_FMA(-xn, kMp2, QT_FMA(-xn, kMp1, x));
+    const double t2 = QT_FMA(-xn, kPp3, y);
+    const double db = QT_FMA(-xn, kPp3, QT_SUB(y, t2));
+    const double b = QT_FMA(-xn, kPp4, t2);
+    g.a = b;
+    g.da = QT_ADD(db, QT_FMA(-xn, kPp4, QT_SUB(t2, b)));
+    g.route = (n & 1) | ((n & 2) ? 4 : 0) | (((n + 1) & 2) ? 8 : 0);
+  }
+  return g;
+}
+
+QT_HD void qt_sincos_eval(double x, const SincosArg& g, double* s_out, double* c_out) {
+  using namespace glibc;
+  const double a = g.a, da = g.da;
+  const double ab = qt_fabs(a);
+  const double u = QT_ADD(ab, kBig);
+  const int row = static_cast<int>(static_cast<uint32_t>(qt_bits(u)));
+  double sn, ssn, cs, ccs;
+  glibc_sincos_tab(row, &sn, &ssn, &cs, &ccs);
+  const double xr = QT_SUB(ab, QT_SUB(u, kBig));
+  // do_sin(a, da)
+  double S;
+  if (ab < kTaylorMax) {
+    const double xx = QT_MUL(a, a);
+    const double p = QT_FMA(QT_FMA(QT_FMA(QT_FMA(kS5, xx, kS4), xx, kS3), xx, kS2), xx, kS1);
+    S = QT_ADD(a, QT_FMA(xx, QT_FMA(p, a, -QT_MUL(0.5, da)), da));
+  } else {
+    const double d = a <= 0.0 ? -da : da;
+    const double xx = QT_MUL(xr, xr);
+    const double s = QT_ADD(QT_FMA(QT_MUL(xr, xx), QT_FMA(xx, kSn5, kSn3), d), xr);
+    const double c = QT_FMA(d, xr, QT_MUL(xx, QT_FMA(QT_FMA(xx, kCs6, kCs4), xx, kCs2)));
+    const double cor = QT_FMA(s, cs, QT_FMA(-c, sn, QT_FMA(s, ccs, ssn)));
+    S = qt_copysign(QT_ADD(cor, sn), a);
+  }
+  // do_cos(a, da)
+  double C;
+  {
+    const double d = a < 0.0 ? -da : da;
+    const double xc = QT_ADD(xr, d);
+    const double xx = QT_MUL(xc, xc);
+    const double s = QT_FMA(QT_MUL(xc, xx), QT_FMA(xx, kSn5, kSn3), xc);
+    const double c = QT_MUL(xx, QT_FMA(QT_FMA(xx, kCs6, kCs4), xx, kCs2));
+    const double cor = QT_FMA(-s, sn, QT_FMA(-c, cs, QT_FMA(-s, ssn, ccs)));
+    C = QT_ADD(cs, cor);
+  }
+  double sv = (g.route & 1) ? C : S;
+  double cv = (g.route & 1) ? S : C;
+  if (g.route & 4) sv = -sv;
+  if (g.route & 8) cv = -cv;
+  if (g.route & 16) sv = qt_copysign(sv, x);
+  *s_out = g.tiny ? x : sv;
+  *c_out = g.tiny ? 1.0 : cv;
+}
+
+QT_HD void qt_sincos_2pi(double x, double* s_out, double* c_out) {
+  qt_sincos_eval(x, qt_sincos_arg(x), s_out, c_out);
 }
 
 }  // namespace qt

@@ -19,6 +19,7 @@ the classes below (errors.hpp:9-21); device failures -> NumericError("cuda: ..."
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import enum
 import math
 import os
@@ -489,6 +490,14 @@ def fast_bounds_check() -> np.ndarray:
     return out
 
 
+def math_checksum(domain: int) -> np.ndarray:
+    """Device checksums of log / sin / cos over a whole engine domain
+    (0: MRG32k3a, 1: XORWOW); equal to glibc's iff every value is."""
+    out = np.zeros(3, np.uint64)
+    _check(L.lib().qt_math_checksum(int(domain), _u(out)), "math_checksum")
+    return out
+
+
 def uniforms(engine, seed, offset, count) -> np.ndarray:
     out = np.zeros(int(count), np.float64)
     _check(L.lib().qt_uniforms(int(engine), int(seed), int(offset), int(count), _f(out)),
@@ -502,9 +511,107 @@ def uniforms(engine, seed, offset, count) -> np.ndarray:
 NodePayoff = Callable[[int, np.ndarray], float]
 
 
+PAYOFF_PUT, PAYOFF_CALL, PAYOFF_SWING, PAYOFF_MAX_CALL = 0, 1, 2, 3
+
+
+def _rmax(a: float, b: float) -> float:
+    return b if a < b else a  # std::max
+
+
+class Payoff:
+    """A discounted obstacle from the factories below: callable per node like
+    the reference's NodePayoff (bdp.hpp:17), and tabulated for a whole tree in
+    one C-ABI call (qt_payoff_table) by tabulate(). Both evaluate the
+    reference's expressions in its order with the same libm, so the values
+    are bit-identical to the reference factories (pipeline.hpp:120-170)."""
+
+    def __init__(self, kind: int, chain_kind: int, params: TwoFactorParams,
+                 gbm_sigma=(0.2, 0.2, 0.2)):
+        self.kind, self.chain_kind, self.params = kind, chain_kind, params
+        self.gbm_sigma = tuple(float(v) for v in gbm_sigma)
+
+    @staticmethod
+    def _spot(p: TwoFactorParams, t: float, x1: float, x2: float) -> float:
+        # model::spot / spot_compensator / ou_covariance (two_factor.hpp:57-63,144-152)
+        c11 = -math.expm1(-2.0 * p.alpha1 * t) / (2.0 * p.alpha1)
+        c22 = -math.expm1(-2.0 * p.alpha2 * t) / (2.0 * p.alpha2)
+        c12 = -p.rho * math.expm1(-(p.alpha1 + p.alpha2) * t) / (p.alpha1 + p.alpha2)
+        comp = (p.sigma1 * p.sigma1 * c11 + 2.0 * p.sigma1 * p.sigma2 * c12 +
+                p.sigma2 * p.sigma2 * c22)
+        return p.s0 * math.exp(p.sigma1 * x1 + p.sigma2 * x2 - 0.5 * comp)
+
+    def __call__(self, k: int, x) -> float:
+        p = self.params
+        t = k * (p.horizon / p.steps)
+        disc = math.exp(-p.r * t)
+        if self.chain_kind == CHAIN_GBM_3D or self.kind == PAYOFF_MAX_CALL:
+            best = -math.inf
+            for a in range(3):
+                sg = self.gbm_sigma[a]
+                best = _rmax(best, p.s0 * math.exp((p.r - 0.5 * sg * sg) * t + sg * float(x[a])))
+            return disc * _rmax(best - p.strike, 0.0)
+        if self.chain_kind == CHAIN_OU_1D:
+            q = dataclasses.replace(p, sigma2=0.0)
+            sp = self._spot(q, t, float(x[0]), 0.0)
+        elif self.chain_kind == CHAIN_BROWNIAN_1D:
+            sp = p.s0 * math.exp((p.r - 0.5 * p.sigma1 * p.sigma1) * t + p.sigma1 * float(x[0]))
+        else:
+            sp = self._spot(p, t, float(x[0]), float(x[1]))
+        if self.kind == PAYOFF_PUT:
+            return disc * _rmax(p.strike - sp, 0.0)
+        if self.kind == PAYOFF_CALL:
+            return disc * _rmax(sp - p.strike, 0.0)
+        return disc * (sp - p.strike)
+
+    def table(self, tree: "QuantTree") -> np.ndarray:
+        phi = np.zeros(int(tree.sizes.sum()), np.float64)
+        pts = np.ascontiguousarray(np.concatenate([g.data() for g in tree.grids]), np.float64)
+        sig = (C.c_double * 3)(*self.gbm_sigma)
+        _check(L.lib().qt_payoff_table(self.kind, self.chain_kind, C.byref(self.params.c()), sig,
+                                       tree.layers(), _u(tree.sizes), _f(pts), _f(phi)),
+               "payoff_table")
+        return phi
+
+
+def _chain_kind_for_dim(dim: int) -> int:
+    if dim not in (1, 2):
+        raise ValueError("payoff: the reference factories take dim 1 or 2")
+    return CHAIN_BROWNIAN_1D if dim == 1 else CHAIN_TWO_FACTOR
+
+
+def make_put_payoff(params: TwoFactorParams, dim: int) -> Payoff:
+    """pipeline.hpp:123-136: dim 1 = lognormal benchmark put, dim 2 = 2-factor spot put."""
+    return Payoff(PAYOFF_PUT, _chain_kind_for_dim(dim), params)
+
+
+def make_call_payoff(params: TwoFactorParams, dim: int) -> Payoff:
+    """pipeline.hpp:138-151."""
+    return Payoff(PAYOFF_CALL, _chain_kind_for_dim(dim), params)
+
+
+def make_swing_payoff(params: TwoFactorParams, dim: int) -> Payoff:
+    """pipeline.hpp:153-170: discounted signed spread v_k."""
+    return Payoff(PAYOFF_SWING, _chain_kind_for_dim(dim), params)
+
+
+def make_ou_swing_payoff(params: TwoFactorParams) -> Payoff:
+    """Config 3 (new): v_k = e^{-rt} (spot(p, t, x, 0) - K) with sigma2 = 0 on the
+    OuChain1d state (two_factor.hpp:150-152,172-176)."""
+    return Payoff(PAYOFF_SWING, CHAIN_OU_1D, params)
+
+
+def make_max_call_payoff(params: TwoFactorParams, sigma=(0.2, 0.2, 0.2)) -> Payoff:
+    """Config 5 (new): e^{-rt} max(max_a s0 e^{(r - sigma_a^2/2) t + sigma_a x_a} - K, 0)
+    on the GbmChain3d state."""
+    return Payoff(PAYOFF_MAX_CALL, CHAIN_GBM_3D, params, sigma)
+
+
 def tabulate(tree: QuantTree, payoff) -> np.ndarray:
-    """NodePayoff -> phi laid out like visits. Accepts a callable
-    f(layer, node_coords) (bdp.hpp:17) or an already flat table."""
+    """NodePayoff -> phi laid out like visits. Accepts a Payoff from the
+    factories above (one C-ABI call), a callable f(layer, node_coords)
+    (bdp.hpp:17) or an already flat table."""
+    if isinstance(payoff, Payoff):
+        return payoff.table(tree)
     if not callable(payoff):
         phi = np.ascontiguousarray(payoff, dtype=np.float64)
         if phi.size != int(tree.sizes.sum()):
