@@ -233,11 +233,18 @@ QT_API qt_status qt_bench_nn(uint64_t n, uint64_t queries, uint64_t seed, uint64
 QT_API qt_status qt_save_tree(const char* path, int32_t layers, int32_t dim, const uint64_t* sizes,
                               const double* points_all, uint64_t samples, const uint64_t* visits,
                               const uint64_t* joint, const double* pi, int32_t device_arrays);
-/* Header of a tree file: n, dim, M and (nullable) sizes[0..n], to size the arrays. */
+/* Header of a tree file: n, dim, M and (nullable) sizes[0..n], to size the
+ * arrays; sizes is written only when sizes_cap >= n + 1. Grids of differing dim
+ * are an IoError (the flat layout holds one dim). */
 QT_API qt_status qt_tree_file_info(const char* path, int32_t* layers, int32_t* dim,
-                                   uint64_t* samples, uint64_t* sizes);
-QT_API qt_status qt_load_tree(const char* path, uint64_t* sizes, double* points_all,
-                              uint64_t* visits, uint64_t* joint, double* pi);
+                                   uint64_t* samples, uint64_t* sizes, uint64_t sizes_cap);
+/* Capacities are what the caller allocated: sizes layers + 1, points_all
+ * visits_cap * dim, visits visits_cap, joint and pi joint_cap each; a file that
+ * disagrees (or changed since qt_tree_file_info) is an IoError, nothing past a
+ * capacity is written. */
+QT_API qt_status qt_load_tree(const char* path, int32_t layers, int32_t dim, uint64_t* sizes,
+                              double* points_all, uint64_t* visits, uint64_t visits_cap,
+                              uint64_t* joint, double* pi, uint64_t joint_cap);
 QT_API qt_status qt_save_grid(const char* path, int32_t dim, uint64_t n, const double* pts);
 /* *dim, *n always; pts (nullable) is filled when cap (doubles) >= n * dim. */
 QT_API qt_status qt_load_grid(const char* path, int32_t* dim, uint64_t* n, double* pts,
@@ -281,6 +288,9 @@ QT_API qt_status qt_fast_bounds_check(double* out);
 QT_API qt_status qt_math_checksum(int32_t domain, uint64_t* out);
 
 /* Thread-local text of the last failure on this thread. */
+/* Free the one-call plans qt_estimate caches (device tables plus the joint /
+ * visits / pi result buffers of the last max(2, devices) input sets). */
+QT_API qt_status qt_plan_cache_clear(void);
 QT_API const char* qt_last_error(void);
 /* Build identification: "qtree_cuda <version> sm_100a ..." */
 QT_API const char* qt_version(void);

@@ -62,6 +62,7 @@ _SIGS = {
     "qt_plan_fast_stats": [C.c_void_p, _u64p],
     "qt_fast_bounds_check": [_f64p],
     "qt_math_checksum": [C.c_int32, _u64p],
+    "qt_plan_cache_clear": [],
     "qt_payoff_table": [C.c_int32, C.c_int32, C.POINTER(QtModelParams), _f64p, C.c_int32, _u64p,
                         _f64p, _f64p],
     "qt_lloyd_build": [C.c_int32, C.c_uint64, C.c_int32, C.c_uint64, C.c_uint64, _f64p, C.c_uint64,
@@ -72,8 +73,9 @@ _SIGS = {
     "qt_save_tree": [C.c_char_p, C.c_int32, C.c_int32, _u64p, _f64p, C.c_uint64, C.c_void_p,
                      C.c_void_p, C.c_void_p, C.c_int32],
     "qt_tree_file_info": [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
-                          C.POINTER(C.c_uint64), _u64p],
-    "qt_load_tree": [C.c_char_p, _u64p, _f64p, _u64p, _u64p, _f64p],
+                          C.POINTER(C.c_uint64), _u64p, C.c_uint64],
+    "qt_load_tree": [C.c_char_p, C.c_int32, C.c_int32, _u64p, _f64p, _u64p, C.c_uint64, _u64p,
+                     _f64p, C.c_uint64],
     "qt_save_grid": [C.c_char_p, C.c_int32, C.c_uint64, _f64p],
     "qt_load_grid": [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_uint64), _f64p, C.c_uint64],
 }

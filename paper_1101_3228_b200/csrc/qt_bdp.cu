@@ -203,6 +203,7 @@ void build_csr(int n, const std::vector<uint64_t>& sizes, const double* d_pi,
 
 template <class F>
 qt_status bdp_guarded(F&& f) {
+  qt::DeviceRestore keep_device;
   try {
     f();
     return QT_OK;
@@ -241,7 +242,7 @@ void check_device() {
   int avail = 0;
   if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
     bdp_raise(QT_ERR_DEVICE, "cuda: no CUDA device available (the pricer has no CPU path)");
-  BDP_CUDA(cudaSetDevice(0));
+  // runs on the caller's current device
 }
 
 void check_tree_args(int layers, const uint64_t* sizes, const uint64_t* visits, const double* pi,

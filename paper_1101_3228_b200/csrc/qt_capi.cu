@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <mutex>
 #include <numeric>
 #include <set>
@@ -84,6 +85,7 @@ struct Failure {
 
 template <class F>
 qt_status guarded(F&& f) {
+  qt::DeviceRestore keep_device;  // every entry point leaves the caller's current device as it was
   try {
     f();
     return QT_OK;
@@ -981,13 +983,13 @@ std::unique_ptr<qt_plan> take_plan(const std::vector<uint8_t>& key, const qt_cha
   }
   return std::unique_ptr<qt_plan>(make_plan(chain, grids, device));
 }
-void give_plan(std::vector<uint8_t> key, std::unique_ptr<qt_plan> p) {
+void give_plan(std::vector<uint8_t> key, std::unique_ptr<qt_plan> p, size_t keep) {
   if (fast_enabled()) return;  // fast-path plans report their stats on destruction
   if (const char* e = std::getenv("QT_PLAN_CACHE"); e && e[0] == '0') return;
   PlanCache& c = plan_cache();
   std::lock_guard<std::mutex> lk(c.mu);
   c.items.emplace_back(std::move(key), std::move(p));
-  while (c.items.size() > kPlanCacheSize) c.items.erase(c.items.begin());
+  while (c.items.size() > std::max(kPlanCacheSize, keep)) c.items.erase(c.items.begin());
 }
 
 int source_of(int engine, bool normals_in) {
@@ -1266,19 +1268,21 @@ const Nccl& nccl() {
   });
   return n;
 }
-// One communicator clique per device count, created on first use and kept
-// (ncclCommInitAll costs far more than a C2-sized all-reduce); calls that use
-// the same clique are serialised by its mutex. Never destroyed (process exit).
+// One communicator clique per device range (first device, count), created on
+// first use and kept (ncclCommInitAll costs far more than a C2-sized
+// all-reduce); calls that use the same clique are serialised by its mutex. A
+// clique whose collective failed is destroyed and re-created by the next call.
+// Never destroyed otherwise (process exit).
 struct NcclClique {
   std::mutex mu;
   std::vector<void*> comms;
 };
-NcclClique& nccl_clique(int G) {
+NcclClique& nccl_clique(int base, int G) {
   static std::mutex m;
-  static std::vector<std::unique_ptr<NcclClique>>* cliques =
-      new std::vector<std::unique_ptr<NcclClique>>(65);
+  static std::map<std::pair<int, int>, std::unique_ptr<NcclClique>>* cliques =
+      new std::map<std::pair<int, int>, std::unique_ptr<NcclClique>>;
   std::lock_guard<std::mutex> lk(m);
-  auto& c = (*cliques)[static_cast<size_t>(G)];
+  auto& c = (*cliques)[{base, G}];
   if (!c) c = std::make_unique<NcclClique>();
   return *c;
 }
@@ -1353,9 +1357,13 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
   int avail = 0;
   if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
     raise(QT_ERR_DEVICE, "cuda: no CUDA device available (the estimator has no CPU path)");
-  if (devices > avail)
+  // devices base .. base + G - 1, base = the caller's current device (a torchrun
+  // rank that did set_device(local_rank) estimates on its own GPU)
+  const int base = qt::current_device();
+  if (base + devices > avail)
     raise(QT_ERR_INVALID_ARGUMENT, "estimate: requested " + std::to_string(devices) +
-                                       " devices, " + std::to_string(avail) + " present");
+                                       " devices from device " + std::to_string(base) + ", " +
+                                       std::to_string(avail) + " present");
   if (h_normals && devices != 1) raise(QT_ERR_INVALID_ARGUMENT, "normals mode is single-device");
   check_inputs(chain, grids);
   const int n = chain->layers;
@@ -1374,12 +1382,12 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
   double* d_pi = nullptr;
   auto cleanup = [&] {
     for (int g = 0; g < G; ++g) {
-      cudaSetDevice(g);
+      cudaSetDevice(base + g);
       if (streams[g]) cudaStreamDestroy(streams[g]);
       for (int e = 0; e < 4; ++e)
         if (ev[4 * g + e]) cudaEventDestroy(ev[4 * g + e]);
     }
-    cudaSetDevice(0);
+    cudaSetDevice(base);
     cudaFree(d_normals);
   };
   const bool dbg = std::getenv("QT_DEBUG") != nullptr;
@@ -1387,11 +1395,11 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
     if (dbg) std::fprintf(stderr, "qtree: %-12s %9.2f ms\n", what, ms_since(t0));
   };
   try {
-    for (int g = 0; g < G; ++g) keys[g] = plan_key(chain, grids, g);
+    for (int g = 0; g < G; ++g) keys[g] = plan_key(chain, grids, base + g);
     for (int g = 0; g < G; ++g) {
-      plans[g] = take_plan(keys[g], chain, grids, g);
+      plans[g] = take_plan(keys[g], chain, grids, base + g);
       mark("plan");
-      QT_CUDA(cudaSetDevice(g));
+      QT_CUDA(cudaSetDevice(base + g));
       QT_CUDA(cudaStreamCreateWithFlags(&streams[g], cudaStreamNonBlocking));
       for (int e = 0; e < 4; ++e) QT_CUDA(cudaEventCreate(&ev[4 * g + e]));
       if (!plans[g]->d_ojoint)
@@ -1402,7 +1410,7 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
     if (h_normals) {
       const uint64_t per = alg == QT_ALG_III ? static_cast<uint64_t>(plans[0]->dim + plans[0]->nps)
                                              : static_cast<uint64_t>(n) * plans[0]->nps;
-      QT_CUDA(cudaSetDevice(0));
+      QT_CUDA(cudaSetDevice(base));
       QT_CUDA(cudaMalloc(&d_normals, count * per * sizeof(double)));
       QT_CUDA(cudaMemcpyAsync(d_normals, h_normals, count * per * sizeof(double),
                               cudaMemcpyHostToDevice, streams[0]));
@@ -1412,7 +1420,7 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
     for (int g = 0; g < G; ++g) {
       const uint64_t b = first + static_cast<uint64_t>(static_cast<u128>(count) * g / G);
       const uint64_t e = first + static_cast<uint64_t>(static_cast<u128>(count) * (g + 1) / G);
-      QT_CUDA(cudaSetDevice(g));
+      QT_CUDA(cudaSetDevice(base + g));
       QT_CUDA(cudaEventRecord(ev[4 * g], streams[g]));
       plan_count(plans[g].get(), alg, engine, seed, b, e - b, total, d_normals, dj[g], streams[g]);
       QT_CUDA(cudaEventRecord(ev[4 * g + 1], streams[g]));
@@ -1428,33 +1436,42 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
       const Nccl& nc = nccl();
       if (!nc.ok) raise(QT_ERR_DEVICE, "nccl: libnccl.so.2 not loadable for devices > 1");
       if (G > 64) raise(QT_ERR_INVALID_ARGUMENT, "estimate: at most 64 devices");
-      NcclClique& cq = nccl_clique(G);
+      NcclClique& cq = nccl_clique(base, G);
       std::lock_guard<std::mutex> clk(cq.mu);
       int rc = 0;
       if (cq.comms.empty()) {
         std::vector<void*> comms(G);
         std::vector<int> devs(G);
-        std::iota(devs.begin(), devs.end(), 0);
+        std::iota(devs.begin(), devs.end(), base);
         rc = nc.init_all(comms.data(), G, devs.data());
         if (rc) raise(QT_ERR_DEVICE, std::string("nccl: ") + (nc.err ? nc.err(rc) : "init failed"));
         cq.comms = comms;
       }
-      nc.group_start();
-      for (int g = 0; g < G; ++g) {
-        cudaSetDevice(g);
-        nc.all_reduce(dj[g], dj[g], plans[g]->njoint, kNcclUint64, kNcclSum, cq.comms[g], streams[g]);
+      rc = nc.group_start();
+      int rc_ar = 0;
+      for (int g = 0; g < G && rc == 0; ++g) {
+        cudaSetDevice(base + g);
+        const int r = nc.all_reduce(dj[g], dj[g], plans[g]->njoint, kNcclUint64, kNcclSum,
+                                    cq.comms[g], streams[g]);
+        if (r && !rc_ar) rc_ar = r;
       }
-      rc = nc.group_end();
+      if (rc == 0) rc = nc.group_end();
+      if (rc == 0) rc = rc_ar;
       for (int g = 0; g < G; ++g) {
-        cudaSetDevice(g);
+        cudaSetDevice(base + g);
         cudaEventRecord(ev[4 * g + 2], streams[g]);
         cudaStreamSynchronize(streams[g]);
+      }
+      if (rc) {  // a communicator that saw an error is not reused
+        for (void* c : cq.comms)
+          if (c) nc.destroy(c);
+        cq.comms.clear();
       }
       if (rc) raise(QT_ERR_DEVICE, std::string("nccl: ") + (nc.err ? nc.err(rc) : "all-reduce failed"));
     } else {
       QT_CUDA(cudaEventRecord(ev[2], streams[0]));
     }
-    QT_CUDA(cudaSetDevice(0));
+    QT_CUDA(cudaSetDevice(base));
     qt_plan* p0 = plans[0].get();
     if (!p0->d_ovis) QT_CUDA(cudaMalloc(&p0->d_ovis, p0->nvis * sizeof(uint64_t)));
     if (!p0->d_opi) QT_CUDA(cudaMalloc(&p0->d_opi, p0->njoint * sizeof(double)));
@@ -1485,11 +1502,11 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
       float count_ms = 0, merge_ms = 0, norm_ms = 0;
       for (int g = 0; g < G; ++g) {
         float c = 0;
-        cudaSetDevice(g);
+        cudaSetDevice(base + g);
         cudaEventElapsedTime(&c, ev[4 * g], ev[4 * g + 1]);
         count_ms = std::max(count_ms, c);
       }
-      cudaSetDevice(0);
+      cudaSetDevice(base);
       cudaEventElapsedTime(&merge_ms, ev[1], ev[2]);
       cudaEventElapsedTime(&norm_ms, ev[2], ev[3]);
       phases[0] = 0.0;       // simulate: fused into the path kernel, reported under nn
@@ -1504,7 +1521,7 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
   }
   cleanup();
   for (int g = 0; g < G; ++g)
-    if (plans[g]) give_plan(std::move(keys[g]), std::move(plans[g]));
+    if (plans[g]) give_plan(std::move(keys[g]), std::move(plans[g]), static_cast<size_t>(G));
 }
 
 }  // namespace
@@ -1812,9 +1829,9 @@ QT_API qt_status qt_lloyd_build(int32_t dim, uint64_t n_points, int32_t iteratio
     int avail = 0;
     if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
       raise(QT_ERR_DEVICE, "cuda: no CUDA device available (the build has no CPU path)");
-    QT_CUDA(cudaSetDevice(0));
+    const int dev0 = qt::current_device();  // the caller's device
     const uint64_t d = static_cast<uint64_t>(dim), N = n_points, M = samples_per_iter;
-    const qt::SrcArgs src = make_src(0, QT_ENGINE_MRG32K3A, stream_seed, 1, 1, nullptr, 0);
+    const qt::SrcArgs src = make_src(dev0, QT_ENGINE_MRG32K3A, stream_seed, 1, 1, nullptr, 0);
     cudaStream_t st = nullptr;
     std::vector<void*> bufs;
     auto dalloc = [&](size_t bytes) {
@@ -1931,8 +1948,8 @@ QT_API qt_status qt_bench_pi(int32_t engine, uint64_t seed, uint64_t samples, ui
     int avail = 0;
     if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
       raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
-    QT_CUDA(cudaSetDevice(0));
-    const qt::SrcArgs a = make_src(0, engine, seed, 1, 1, nullptr, 0);
+    const int dev0 = qt::current_device();  // the caller's device
+    const qt::SrcArgs a = make_src(dev0, engine, seed, 1, 1, nullptr, 0);
     unsigned long long* d = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     auto fin = [&] {
@@ -1978,8 +1995,8 @@ QT_API qt_status qt_bench_nn(uint64_t n, uint64_t queries, uint64_t seed, uint64
     int avail = 0;
     if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
       raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
-    QT_CUDA(cudaSetDevice(0));
-    const qt::SrcArgs a = make_src(0, QT_ENGINE_MRG32K3A, seed, 1, 1, nullptr, 0);
+    const int dev0 = qt::current_device();  // the caller's device
+    const qt::SrcArgs a = make_src(dev0, QT_ENGINE_MRG32K3A, seed, 1, 1, nullptr, 0);
     std::vector<void*> bufs;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     auto fin = [&] {
@@ -2041,7 +2058,6 @@ QT_API qt_status qt_nearest(int32_t dim, uint64_t n_points, const double* points
       raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
     const GridTables gt = grid_tables(dim, n_points, points);
     const std::vector<uint8_t>& t = gt.blob;
-    QT_CUDA(cudaSetDevice(0));
     uint8_t* d_t = nullptr;
     double* d_q = nullptr;
     unsigned long long* d_o = nullptr;
@@ -2075,8 +2091,8 @@ QT_API qt_status qt_path_normals(int32_t engine, uint64_t seed, uint64_t normals
     int avail = 0;
     if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
       raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
-    QT_CUDA(cudaSetDevice(0));
-    auto a = make_src(0, engine, seed, 2 * ((normals_per_path + 1) / 2),
+    const int dev0 = qt::current_device();  // the caller's device
+    auto a = make_src(dev0, engine, seed, 2 * ((normals_per_path + 1) / 2),
                       static_cast<uint32_t>(normals_per_path), nullptr, 0);
     double* d = nullptr;
     QT_CUDA(cudaMalloc(&d, count * normals_per_path * sizeof(double)));
@@ -2098,8 +2114,8 @@ QT_API qt_status qt_uniforms(int32_t engine, uint64_t seed, uint64_t offset, uin
     int avail = 0;
     if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
       raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
-    QT_CUDA(cudaSetDevice(0));
-    auto a = make_src(0, engine, seed, 1, 1, nullptr, 0);
+    const int dev0 = qt::current_device();  // the caller's device
+    auto a = make_src(dev0, engine, seed, 1, 1, nullptr, 0);
     double* d = nullptr;
     QT_CUDA(cudaMalloc(&d, count * sizeof(double)));
     cudaError_t e = qt::launch_uniforms(engine, a, offset, count, d, nullptr);
@@ -2145,7 +2161,6 @@ QT_API qt_status qt_fast_bounds_check(double* out) {
     int avail = 0;
     if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
       raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
-    QT_CUDA(cudaSetDevice(0));
     unsigned int* d = nullptr;
     QT_CUDA(cudaMalloc(&d, 4 * sizeof(unsigned int)));
     cudaError_t e = cudaMemset(d, 0, 4 * sizeof(unsigned int));
@@ -2180,6 +2195,20 @@ QT_API qt_status qt_math_checksum(int32_t domain, uint64_t* out) {
     QT_CUDA(e);
     g_launches.fetch_add(1);
     for (int i = 0; i < 3; ++i) out[i] = h[i];
+  });
+}
+
+// Frees every cached one-call plan (tables and the joint / visits / pi result
+// buffers) on whatever device each lives on.
+QT_API qt_status qt_plan_cache_clear(void) {
+  return guarded([&] {
+    std::vector<std::pair<std::vector<uint8_t>, std::unique_ptr<qt_plan>>> drop;
+    {
+      PlanCache& c = plan_cache();
+      std::lock_guard<std::mutex> lk(c.mu);
+      drop.swap(c.items);
+    }
+    drop.clear();
   });
 }
 

@@ -10,6 +10,34 @@
 
 namespace qt {
 
+// The caller's current CUDA device (0 when the runtime has none to report).
+inline int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) {
+    cudaGetLastError();
+    d = 0;
+  }
+  return d;
+}
+
+// Saves the current device on entry to a C-ABI call and restores it on exit,
+// so no entry point (nor a plan destructor it triggers) changes the caller's
+// device. No-op when there is no device.
+struct DeviceRestore {
+  int dev = -1;
+  DeviceRestore() {
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      cudaGetLastError();
+      dev = -1;
+    }
+  }
+  ~DeviceRestore() {
+    if (dev >= 0) cudaSetDevice(dev);
+  }
+  DeviceRestore(const DeviceRestore&) = delete;
+  DeviceRestore& operator=(const DeviceRestore&) = delete;
+};
+
 // Normal-source parameters (see Source<> in qt_device.cuh).
 struct SrcArgs {
   uint32_t mrg_seed[6];

@@ -219,9 +219,12 @@ QT_API qt_status qt_save_tree(const char* path, int32_t layers, int32_t dim, con
 }
 
 // The header of a tree file and its total sizes: layers n, dim, M and sizes[0..n]
-// (nullable), so a caller can allocate the arrays qt_load_tree fills.
+// (nullable; written only when sizes_cap >= n + 1), so a caller can allocate the
+// arrays qt_load_tree fills. Every embedded grid must have the first grid's dim
+// (the flat layout holds one dim; the reference's make_tree_shell requires it,
+// estimate.hpp:55-58).
 QT_API qt_status qt_tree_file_info(const char* path, int32_t* layers, int32_t* dim,
-                                   uint64_t* samples, uint64_t* sizes) {
+                                   uint64_t* samples, uint64_t* sizes, uint64_t sizes_cap) {
   return io_guarded([&] {
     if (!path) fail(QT_ERR_INVALID_ARGUMENT, "load_tree: null path");
     const std::string p(path);
@@ -247,8 +250,10 @@ QT_API qt_status qt_tree_file_info(const char* path, int32_t* layers, int32_t* d
       TextGrid tg;
       if (!parse_grid(text.data(), text.data() + text.size(), tg, true))
         fail(QT_ERR_IO, "tree file: malformed embedded grid");
-      d = tg.dim;
-      if (sizes) sizes[k] = tg.pts.size() / static_cast<uint64_t>(tg.dim);
+      if (k == 0) d = tg.dim;
+      else if (tg.dim != d) fail(QT_ERR_IO, "load_tree: grids of differing dimension in " + p);
+      if (sizes && sizes_cap >= static_cast<uint64_t>(n) + 1)
+        sizes[k] = tg.pts.size() / static_cast<uint64_t>(tg.dim);
     }
     if (layers) *layers = static_cast<int32_t>(n);
     if (dim) *dim = d;
@@ -257,11 +262,16 @@ QT_API qt_status qt_tree_file_info(const char* path, int32_t* layers, int32_t* d
 }
 
 // load_tree (quant_tree.hpp:165-205) into caller-allocated host arrays laid out
-// like qt_estimate's (points_all includes layer 0).
-QT_API qt_status qt_load_tree(const char* path, uint64_t* sizes, double* points_all,
-                              uint64_t* visits, uint64_t* joint, double* pi) {
+// like qt_estimate's (points_all includes layer 0). The caller states what it
+// allocated (from qt_tree_file_info): sizes holds layers + 1 entries,
+// points_all visits_cap * dim doubles, visits visits_cap, joint and pi
+// joint_cap each. A file that needs more (or changed since the info call)
+// fails with QT_ERR_IO before anything past a capacity is written.
+QT_API qt_status qt_load_tree(const char* path, int32_t layers, int32_t dim, uint64_t* sizes,
+                              double* points_all, uint64_t* visits, uint64_t visits_cap,
+                              uint64_t* joint, double* pi, uint64_t joint_cap) {
   return io_guarded([&] {
-    if (!path || !sizes || !points_all || !visits || !joint || !pi)
+    if (!path || !sizes || !points_all || !visits || !joint || !pi || layers < 1 || dim < 1)
       fail(QT_ERR_INVALID_ARGUMENT, "load_tree: null argument");
     const std::string p(path);
     File in;
@@ -275,6 +285,9 @@ QT_API qt_status qt_load_tree(const char* path, uint64_t* sizes, double* points_
     if (version != kVersion) fail(QT_ERR_IO, "load_tree: unsupported version " + std::to_string(version));
     get(in.f, &n, 4);
     if (n == 0) fail(QT_ERR_IO, "load_tree: empty tree");
+    if (n != static_cast<uint32_t>(layers))
+      fail(QT_ERR_IO, "load_tree: " + p + " has " + std::to_string(n) + " layers, caller allocated " +
+                          std::to_string(layers));
     uint64_t m = 0;
     get(in.f, &m, 8);
     double* g = points_all;
@@ -287,8 +300,10 @@ QT_API qt_status qt_load_tree(const char* path, uint64_t* sizes, double* points_
       TextGrid tg;
       if (!parse_grid(text.data(), text.data() + text.size(), tg, true))
         fail(QT_ERR_IO, "tree file: malformed embedded grid");
+      if (tg.dim != dim) fail(QT_ERR_IO, "load_tree: grids of differing dimension in " + p);
       const uint64_t N = tg.pts.size() / static_cast<uint64_t>(tg.dim);
       check_points(tg.dim, N, tg.pts.data(), "grid");
+      if (N > visits_cap - nvis) fail(QT_ERR_IO, "load_tree: " + p + " exceeds the caller's capacity");
       sizes[k] = N;
       std::memcpy(g, tg.pts.data(), tg.pts.size() * 8);
       g += tg.pts.size();
@@ -302,6 +317,7 @@ QT_API qt_status qt_load_tree(const char* path, uint64_t* sizes, double* points_
       get(in.f, &c, 8);
       if (r != sizes[k - 1] || c != sizes[k])
         fail(QT_ERR_IO, "load_tree: transition dimensions disagree with grids");
+      if (r * c > joint_cap - off) fail(QT_ERR_IO, "load_tree: " + p + " exceeds the caller's capacity");
       get(in.f, joint + off, r * c * 8);
       get(in.f, pi + off, r * c * 8);
       off += r * c;

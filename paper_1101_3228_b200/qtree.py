@@ -409,17 +409,17 @@ def save_tree(tree: QuantTree, path) -> None:
 def load_tree(path) -> QuantTree:
     n, d, m = C.c_int32(0), C.c_int32(0), C.c_uint64(0)
     _check(L.lib().qt_tree_file_info(str(path).encode(), C.byref(n), C.byref(d), C.byref(m),
-                                     None), "load_tree")
+                                     None, 0), "load_tree")
     sizes = np.zeros(n.value + 1, np.uint64)
     _check(L.lib().qt_tree_file_info(str(path).encode(), C.byref(n), C.byref(d), C.byref(m),
-                                     _u(sizes)), "load_tree")
+                                     _u(sizes), sizes.size), "load_tree")
     nvis, njoint = layout(sizes)
     pts = np.zeros(nvis * d.value, np.float64)
     v = np.zeros(nvis, np.uint64)
     j = np.zeros(njoint, np.uint64)
     p = np.zeros(njoint, np.float64)
-    _check(L.lib().qt_load_tree(str(path).encode(), _u(sizes), _f(pts), _u(v), _u(j), _f(p)),
-           "load_tree")
+    _check(L.lib().qt_load_tree(str(path).encode(), n.value, d.value, _u(sizes), _f(pts), _u(v),
+                                nvis, _u(j), _f(p), njoint), "load_tree")
     grids, o = [], 0
     for s in sizes:
         grids.append(QuantGrid(d.value, pts[o:o + int(s) * d.value]))

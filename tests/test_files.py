@@ -127,3 +127,55 @@ def test_device_tree_writer_equals_host_writer(gpu, tmp_path, reference):
     ref = tmp_path / "ref.qtre"
     reference.save_tree(ref, 1, t.sizes, _flat(t), M, t.flat_visits, t.flat_joint, t.flat_pi)
     assert dev.read_bytes() == ref.read_bytes()
+
+
+def _qtre(samples, grids_text, visits, mats):
+    """Raw QTRE v1 bytes (quant_tree.hpp:138-163) from explicit parts, to build
+    files the reference's own writer cannot produce."""
+    import struct
+    b = b"QTRE" + struct.pack("<IIQ", 1, len(grids_text) - 1, samples)
+    for t in grids_text:
+        b += struct.pack("<Q", len(t)) + t.encode()
+    b += np.asarray(visits, np.uint64).tobytes()
+    for r, c, j, p in mats:
+        b += struct.pack("<QQ", r, c) + np.asarray(j, np.uint64).tobytes() + \
+            np.asarray(p, np.float64).tobytes()
+    return b
+
+
+def test_tree_load_rejects_mixed_dims_and_overflow(tmp_path):
+    """A malformed file whose grids differ in dim (grid 0 of dim 8, grid 1 of
+    dim 1) used to size the caller's buffers from the last grid and overflow
+    them; it is an IoError now, and the loader never writes past what the
+    caller says it allocated."""
+    q = Q()
+    g0 = "1 8\n" + " ".join(["0"] * 8) + "\n"
+    g1 = "2 1\n0.5\n1.5\n"
+    p = tmp_path / "mixed.qtre"
+    p.write_bytes(_qtre(7, [g0, g1], [7, 3, 4], [(1, 2, [3, 4], [3 / 7, 4 / 7])]))
+    with pytest.raises(q.IoError, match="differing dimension"):
+        q.load_tree(p)
+    # consistent file, but the caller's capacities are too small
+    good = tmp_path / "good.qtre"
+    good.write_bytes(_qtre(7, ["1 1\n0\n", g1], [7, 3, 4], [(1, 2, [3, 4], [3 / 7, 4 / 7])]))
+    import ctypes as C
+    from paper_1101_3228_b200 import _lib
+    lib = _lib.lib()
+    sizes = np.zeros(2, np.uint64)
+    pts = np.full(3, -1.0)
+    v = np.zeros(3, np.uint64)
+    j = np.zeros(2, np.uint64)
+    pi = np.zeros(2)
+
+    def load(layers, vcap, jcap):
+        return lib.qt_load_tree(str(good).encode(), layers, 1, sizes.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                pts.ctypes.data_as(C.POINTER(C.c_double)),
+                                v.ctypes.data_as(C.POINTER(C.c_uint64)), vcap,
+                                j.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                pi.ctypes.data_as(C.POINTER(C.c_double)), jcap)
+    assert load(1, 3, 2) == 0 and list(v) == [7, 3, 4] and list(j) == [3, 4]
+    assert load(2, 3, 2) == 3            # layer count disagrees with the caller's
+    pts[:] = -1.0
+    assert load(1, 2, 2) == 3 and pts[2] == -1.0   # visits capacity: nothing past it
+    assert load(1, 3, 1) == 3
+    q.load_tree(good)
