@@ -18,6 +18,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libqtree_cuda.so")
+# development hook: load a variant build (e.g. other -D tuning flags) instead
+LIB = os.environ.get("QT_LIB_VARIANT") or LIB
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
@@ -49,6 +51,8 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    if os.environ.get("QT_LIB_VARIANT"):
+        return LIB
     if not force and up_to_date():
         return LIB
     import fcntl

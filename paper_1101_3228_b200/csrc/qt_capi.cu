@@ -63,7 +63,7 @@ bool fast_enabled() {
   int v = g_fast.load();
   if (v < 0) {
     const char* e = std::getenv("QT_FAST_PATH");
-    v = (e && e[0] == '1') ? 1 : 0;  // TEMP default off until it beats k_paths
+    v = (e && e[0] == '0') ? 0 : 1;
     g_fast.store(v);
   }
   return v == 1;
@@ -508,8 +508,12 @@ std::vector<uint8_t> build_fast_table(int kind, const std::vector<double>& t,
     r.tl = c ? f32_up(t[c - 1]) : -inf;
     r.t0 = f32_down(t[c]);
     r.t1 = c + 1 < N ? f32_down(t[c + 1]) : inf;
-    r.o0 = static_cast<uint16_t>(ord[c]);
-    r.o1 = static_cast<uint16_t>(ord[std::min<uint64_t>(c + 1, N - 1)]);
+    // sorted positions: the certified counts land in sorted-cell space, where a
+    // layer's hits crowd a band around the diagonal (Brownian steps are small
+    // against the grid), so the count array's hot lines stay L2-resident
+    (void)ord;
+    r.o0 = static_cast<uint16_t>(c);
+    r.o1 = static_cast<uint16_t>(std::min<uint64_t>(c + 1, N - 1));
     R[b] = r;
   }
   return out;
@@ -984,7 +988,6 @@ std::unique_ptr<qt_plan> take_plan(const std::vector<uint8_t>& key, const qt_cha
   return std::unique_ptr<qt_plan>(make_plan(chain, grids, device));
 }
 void give_plan(std::vector<uint8_t> key, std::unique_ptr<qt_plan> p, size_t keep) {
-  if (fast_enabled()) return;  // fast-path plans report their stats on destruction
   if (const char* e = std::getenv("QT_PLAN_CACHE"); e && e[0] == '0') return;
   PlanCache& c = plan_cache();
   std::lock_guard<std::mutex> lk(c.mu);
@@ -1024,7 +1027,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
     a.layers_per_stage = 1;
     const bool resident = p->total_tab <= kResidentBudget;
     const size_t smem = resident ? p->total_tab : static_cast<size_t>(p->stages) * p->max_tab;
-    const bool fast = fast_enabled() && src == QT_ENGINE_MRG32K3A && p->d_ftables &&
+    const bool fast = fast_enabled() && src == QT_ENGINE_MRG32K3A && p->d_ftables && p->d_orig &&
                       (p->kind == QT_CHAIN_BROWNIAN_1D || p->kind == QT_CHAIN_OU_1D) &&
                       p->n < 65536 && first + count <= (1ull << 48);
     if (fast) {
@@ -1066,16 +1069,21 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       const uint64_t T = blocks * slots_per_block;
       fa_args.q = count / T;
       fa_args.rem = count % T;
+      if (!p->d_sjoint) QT_CUDA(cudaMalloc(&p->d_sjoint, p->njoint * sizeof(uint64_t)));
+      QT_CUDA(cudaMemsetAsync(p->d_sjoint, 0, p->njoint * sizeof(uint64_t), st));
       qt::FastArgs fa{fa_args, p->d_amb, p->d_stats, std::min(p->amb_cap, want),
                       p->d_ftables, p->d_ftab_off, p->d_ftab_bytes, fbuf, p->total_ftab,
-                      st_n, {}, std::getenv("QT_PROBE_NORED") ? 1u : 0u};
+                      st_n, {}, std::getenv("QT_PROBE_NORED") ? 1u : 0u, p->d_sjoint};
       mrg_back_jump(2 * ((static_cast<uint64_t>(p->n) + 1) / 2), fa.back);
       QT_CUDA(cudaMemsetAsync(p->d_stats, 0, sizeof(unsigned long long), st));
       QT_CUDA(qt::launch_paths_fast(p->kind, fres, P, fa, static_cast<uint32_t>(blocks), fsmem,
                                     static_cast<uint32_t>(p->sm_count) * 4u, st));
+      QT_CUDA(qt::launch_permute_add(p->d_sjoint, reinterpret_cast<unsigned long long*>(d_joint),
+                                     p->d_fin, p->d_orig, static_cast<uint32_t>(p->n),
+                                     p->max_elems, st));
       p->fast_paths += count;
-      g_launches.fetch_add(2);
-      return 2;
+      g_launches.fetch_add(3);
+      return 3;
     }
     if (src == QT_ENGINE_MRG32K3A && (p->kind == QT_CHAIN_BROWNIAN_1D || p->kind == QT_CHAIN_OU_1D) &&
         xkernel_enabled() && !p->gmem && p->d_xtables) {  // 1-D MRG32k3a: the lockstep exact kernel
@@ -2137,6 +2145,20 @@ QT_API qt_status qt_fast_stats(uint64_t* out) {
     out[0] = g_fast_paths.load();
     out[1] = g_fast_replayed.load();
     out[2] = g_fast_inline.load();
+    // plus the plans still held by the one-call cache (destroyed plans add theirs above)
+    PlanCache& c = plan_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (const auto& it : c.items) {
+      const qt_plan* pl = it.second.get();
+      if (!pl->d_stats) continue;
+      unsigned long long st[3] = {0, 0, 0};
+      QT_CUDA(cudaSetDevice(pl->device));
+      QT_CUDA(cudaDeviceSynchronize());
+      QT_CUDA(cudaMemcpy(st, pl->d_stats, sizeof st, cudaMemcpyDeviceToHost));
+      out[0] += pl->fast_paths;
+      out[1] += st[1];
+      out[2] += st[2];
+    }
   });
 }
 

@@ -71,6 +71,9 @@ struct PathArgs {
 };
 
 constexpr int kPathConsumers = 256;  // consumer threads per k_paths CTA
+#ifndef QT_X_MINB  // k_paths_x: resident CTAs per SM the register allocation must allow
+#define QT_X_MINB 1
+#endif
 #ifndef QT_X_THREADS
 #define QT_X_THREADS 256
 #endif
@@ -97,6 +100,8 @@ struct FastArgs {
   uint32_t fstages;           // prefetch depth (stages of fbuf_bytes)
   uint32_t back[18];          // (J^D)^-1 mod m1 | mod m2: path end -> path start
   uint32_t probe_nored;       // diagnostics only (QT_PROBE_NORED): skip the count REDs
+  unsigned long long* sjoint; // certified counts, SORTED-cell space (launch_permute_add maps
+                              // them to p.joint); replays count into p.joint directly
 };
 
 // d >= 2 FP32-scan path kernel (qt_scan.cu)

@@ -354,9 +354,9 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_fast(const __grid_consta
       } else {
         mbar_wait_u32(full0 + 8u * s, ph);
       }
-      fast_layer<K, P>(ps, act, tb, k, a.joint, f.probe_nored == 0);
+      fast_layer<K, P>(ps, act, tb, k, f.sjoint, f.probe_nored == 0);
       if (k + 1 <= a.n)
-        fast_layer<K, P>(ps, act, tb + __ldg(f.ftab_bytes + k - 1), k + 1, a.joint,
+        fast_layer<K, P>(ps, act, tb + __ldg(f.ftab_bytes + k - 1), k + 1, f.sjoint,
                          f.probe_nored == 0);
       if constexpr (!RESIDENT) {
         named_barrier_sync(1, kFastThreads);  // every thread is done with stage s
@@ -515,7 +515,7 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
 // tables of layers 2q+1 and 2q+2, which share one Box-Muller pair, so the table
 // wait and the barrier are paid once per two layers.
 template <int K, bool RESIDENT, int P, int L>
-__global__ void __launch_bounds__(kXThreads) k_paths_x(const __grid_constant__ PathArgs a) {
+__global__ void __launch_bounds__(kXThreads, QT_X_MINB) k_paths_x(const __grid_constant__ PathArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   const uint32_t tid = threadIdx.x;

@@ -51,6 +51,21 @@ static __device__ const double2 kGlibcLogTabDev[128] = {QT_GLIBC_LOG_TAB};
 // row i = {sn, ssn} at [2i], {cs, ccs} at [2i + 1]
 static __device__ const double2 kGlibcSincosTabDev[220] = {QT_GLIBC_SINCOS_TAB};
 #endif
+// The scalar constants again, as a __constant__ struct on the device: an FP64
+// operand read from the constant bank costs no instruction, where a 64-bit
+// immediate is first materialised into a uniform register pair (two UMOVs per
+// use in the unrolled loops). Same values, same bits.
+struct GlibcConst {
+  double kLn2Hi, kLn2Lo, kA0, kA1, kA2, kA3, kA4, kB0, kB1, kB2, kB3, kB4, kB5, kB6, kB7, kB8, kB9, kB10, kBig, kSn3, kSn5, kCs2, kCs4, kCs6, kS1, kS2, kS3, kS4, kS5, kHp0, kHp1, kTaylorMax, kToint, kHpinv, kMp1, kMp2, kPp3, kPp4;
+};
+#if defined(__CUDACC__)
+static __constant__ GlibcConst kGlibcConstDev = {glibc::kLn2Hi, glibc::kLn2Lo, glibc::kA0, glibc::kA1, glibc::kA2, glibc::kA3, glibc::kA4, glibc::kB0, glibc::kB1, glibc::kB2, glibc::kB3, glibc::kB4, glibc::kB5, glibc::kB6, glibc::kB7, glibc::kB8, glibc::kB9, glibc::kB10, glibc::kBig, glibc::kSn3, glibc::kSn5, glibc::kCs2, glibc::kCs4, glibc::kCs6, glibc::kS1, glibc::kS2, glibc::kS3, glibc::kS4, glibc::kS5, glibc::kHp0, glibc::kHp1, glibc::kTaylorMax, glibc::kToint, glibc::kHpinv, glibc::kMp1, glibc::kMp2, glibc::kPp3, glibc::kPp4};
+#endif
+#if defined(__CUDA_ARCH__)
+#define QT_GK(n) (::qt::kGlibcConstDev.n)
+#else
+#define QT_GK(n) (::qt::glibc::n)
+#endif
 struct GlibcLogEnt {
   double invc, logc;
 };
@@ -113,26 +128,25 @@ QT_HD bool qt_log_near1(double x) { return qt_bits(x) - kLogLo < kLogHiMinusLo; 
 // x in [1 - 2^-4, 1 + 0x1.09p-4): log1p(r), r = x - 1, by the degree-11
 // polynomial plus the exact-ish head r - r^2/2 (e_log.c "close to 1.0").
 QT_HD double qt_log_near1_eval(double x) {
-  using namespace glibc;
   if (qt_bits(x) == 0x3ff0000000000000ull) return 0.0;
   const double r = QT_SUB(x, 1.0);
   const double r2 = QT_MUL(r, r);
   const double r3 = QT_MUL(r, r2);
-  double t7 = QT_FMA(r, kB8, kB7);
-  t7 = QT_FMA(r2, kB9, t7);
-  t7 = QT_FMA(r3, kB10, t7);
-  double t4 = QT_FMA(r, kB5, kB4);
-  t4 = QT_FMA(r2, kB6, t4);
+  double t7 = QT_FMA(r, QT_GK(kB8), QT_GK(kB7));
+  t7 = QT_FMA(r2, QT_GK(kB9), t7);
+  t7 = QT_FMA(r3, QT_GK(kB10), t7);
+  double t4 = QT_FMA(r, QT_GK(kB5), QT_GK(kB4));
+  t4 = QT_FMA(r2, QT_GK(kB6), t4);
   t4 = QT_FMA(t7, r3, t4);
-  double t1 = QT_FMA(r, kB2, kB1);
-  t1 = QT_FMA(r2, kB3, t1);
+  double t1 = QT_FMA(r, QT_GK(kB2), QT_GK(kB1));
+  t1 = QT_FMA(r2, QT_GK(kB3), t1);
   const double p = QT_FMA(t4, r3, t1);
   const double rhi = QT_FMA(-r, 0x1p27, QT_FMA(r, 0x1p27, r));  // (r + w) - w, w = r 2^27
   const double rlo = QT_SUB(r, rhi);
   const double rh2 = QT_MUL(rhi, rhi);
-  const double hi = QT_FMA(rh2, kB0, r);
-  double lo = QT_FMA(rh2, kB0, QT_SUB(r, hi));
-  lo = QT_FMA(QT_MUL(kB0, rlo), QT_ADD(r, rhi), lo);
+  const double hi = QT_FMA(rh2, QT_GK(kB0), r);
+  double lo = QT_FMA(rh2, QT_GK(kB0), QT_SUB(r, hi));
+  lo = QT_FMA(QT_MUL(QT_GK(kB0), rlo), QT_ADD(r, rhi), lo);
   return QT_ADD(hi, QT_FMA(p, r3, lo));
 }
 
@@ -154,14 +168,13 @@ QT_HD LogPrep qt_log_prep(double x) {
   return q;
 }
 QT_HD double qt_log_finish(const LogPrep& q) {
-  using namespace glibc;
   const double r = QT_FMA(q.z, q.invc, -1.0);
-  const double w = QT_FMA(q.kd, kLn2Hi, q.logc);
+  const double w = QT_FMA(q.kd, QT_GK(kLn2Hi), q.logc);
   const double hi = QT_ADD(w, r);
-  const double lo = QT_FMA(q.kd, kLn2Lo, QT_ADD(QT_SUB(w, hi), r));
+  const double lo = QT_FMA(q.kd, QT_GK(kLn2Lo), QT_ADD(QT_SUB(w, hi), r));
   const double r2 = QT_MUL(r, r);
-  const double p = QT_FMA(r2, QT_FMA(r, kA4, kA3), QT_FMA(r, kA2, kA1));
-  const double y = QT_FMA(QT_MUL(r, r2), p, QT_FMA(r2, kA0, lo));
+  const double p = QT_FMA(r2, QT_FMA(r, QT_GK(kA4), QT_GK(kA3)), QT_FMA(r, QT_GK(kA2), QT_GK(kA1)));
+  const double y = QT_FMA(QT_MUL(r, r2), p, QT_FMA(r2, QT_GK(kA0), lo));
   return QT_ADD(y, hi);
 }
 QT_HD double qt_log_unit(double x) {
@@ -186,7 +199,6 @@ struct SincosArg {
   bool tiny;
 };
 QT_HD SincosArg qt_sincos_arg(double x) {
-  using namespace glibc;
   const uint32_t k = static_cast<uint32_t>(qt_bits(x) >> 32) & 0x7fffffffu;
   SincosArg g;
   g.tiny = k < 0x3e400000u;
@@ -195,45 +207,44 @@ QT_HD SincosArg qt_sincos_arg(double x) {
     g.da = 0.0;
     g.route = 0;
   } else if (k < 0x400368fdu) {
-    const double y = QT_SUB(kHp0, qt_fabs(x));
-    g.a = QT_ADD(y, kHp1);
-    g.da = QT_ADD(QT_SUB(y, g.a), kHp1);
+    const double y = QT_SUB(QT_GK(kHp0), qt_fabs(x));
+    g.a = QT_ADD(y, QT_GK(kHp1));
+    g.da = QT_ADD(QT_SUB(y, g.a), QT_GK(kHp1));
     g.route = 1 | 16;  // bit 4: sin takes the sign of x
   } else {
-    const double t = QT_FMA(x, kHpinv, kToint);
-    const double xn = QT_SUB(t, kToint);
+    const double t = QT_FMA(x, QT_GK(kHpinv), QT_GK(kToint));
+    const double xn = QT_SUB(t, QT_GK(kToint));
     const int n = static_cast<int>(qt_bits(t) & 3u);
-    const double y = QT_FMA(-xn, kMp2, QT_FMA(-xn, kMp1, x));
-    const double t2 = QT_FMA(-xn, kPp3, y);
-    const double db = QT_FMA(-xn, kPp3, QT_SUB(y, t2));
-    const double b = QT_FMA(-xn, kPp4, t2);
+    const double y = QT_FMA(-xn, QT_GK(kMp2), QT_FMA(-xn, QT_GK(kMp1), x));
+    const double t2 = QT_FMA(-xn, QT_GK(kPp3), y);
+    const double db = QT_FMA(-xn, QT_GK(kPp3), QT_SUB(y, t2));
+    const double b = QT_FMA(-xn, QT_GK(kPp4), t2);
     g.a = b;
-    g.da = QT_ADD(db, QT_FMA(-xn, kPp4, QT_SUB(t2, b)));
+    g.da = QT_ADD(db, QT_FMA(-xn, QT_GK(kPp4), QT_SUB(t2, b)));
     g.route = (n & 1) | ((n & 2) ? 4 : 0) | (((n + 1) & 2) ? 8 : 0);
   }
   return g;
 }
 
 QT_HD void qt_sincos_eval(double x, const SincosArg& g, double* s_out, double* c_out) {
-  using namespace glibc;
   const double a = g.a, da = g.da;
   const double ab = qt_fabs(a);
-  const double u = QT_ADD(ab, kBig);
+  const double u = QT_ADD(ab, QT_GK(kBig));
   const int row = static_cast<int>(static_cast<uint32_t>(qt_bits(u)));
   double sn, ssn, cs, ccs;
   glibc_sincos_tab(row, &sn, &ssn, &cs, &ccs);
-  const double xr = QT_SUB(ab, QT_SUB(u, kBig));
+  const double xr = QT_SUB(ab, QT_SUB(u, QT_GK(kBig)));
   // do_sin(a, da)
   double S;
-  if (ab < kTaylorMax) {
+  if (ab < QT_GK(kTaylorMax)) {
     const double xx = QT_MUL(a, a);
-    const double p = QT_FMA(QT_FMA(QT_FMA(QT_FMA(kS5, xx, kS4), xx, kS3), xx, kS2), xx, kS1);
+    const double p = QT_FMA(QT_FMA(QT_FMA(QT_FMA(QT_GK(kS5), xx, QT_GK(kS4)), xx, QT_GK(kS3)), xx, QT_GK(kS2)), xx, QT_GK(kS1));
     S = QT_ADD(a, QT_FMA(xx, QT_FMA(p, a, -QT_MUL(0.5, da)), da));
   } else {
     const double d = a <= 0.0 ? -da : da;
     const double xx = QT_MUL(xr, xr);
-    const double s = QT_ADD(QT_FMA(QT_MUL(xr, xx), QT_FMA(xx, kSn5, kSn3), d), xr);
-    const double c = QT_FMA(d, xr, QT_MUL(xx, QT_FMA(QT_FMA(xx, kCs6, kCs4), xx, kCs2)));
+    const double s = QT_ADD(QT_FMA(QT_MUL(xr, xx), QT_FMA(xx, QT_GK(kSn5), QT_GK(kSn3)), d), xr);
+    const double c = QT_FMA(d, xr, QT_MUL(xx, QT_FMA(QT_FMA(xx, QT_GK(kCs6), QT_GK(kCs4)), xx, QT_GK(kCs2))));
     const double cor = QT_FMA(s, cs, QT_FMA(-c, sn, QT_FMA(s, ccs, ssn)));
     S = qt_copysign(QT_ADD(cor, sn), a);
   }
@@ -243,8 +254,8 @@ QT_HD void qt_sincos_eval(double x, const SincosArg& g, double* s_out, double* c
     const double d = a < 0.0 ? -da : da;
     const double xc = QT_ADD(xr, d);
     const double xx = QT_MUL(xc, xc);
-    const double s = QT_FMA(QT_MUL(xc, xx), QT_FMA(xx, kSn5, kSn3), xc);
-    const double c = QT_MUL(xx, QT_FMA(QT_FMA(xx, kCs6, kCs4), xx, kCs2));
+    const double s = QT_FMA(QT_MUL(xc, xx), QT_FMA(xx, QT_GK(kSn5), QT_GK(kSn3)), xc);
+    const double c = QT_MUL(xx, QT_FMA(QT_FMA(xx, QT_GK(kCs6), QT_GK(kCs4)), xx, QT_GK(kCs2)));
     const double cor = QT_FMA(-s, sn, QT_FMA(-c, cs, QT_FMA(-s, ssn, ccs)));
     C = QT_ADD(cs, cor);
   }

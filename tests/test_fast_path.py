@@ -30,11 +30,11 @@ def Q():
 
 @pytest.fixture(autouse=True)
 def fast_on():
-    """The fast path is opt-in: its tables are built by plans created while it
-    is enabled; each test leaves it disabled again."""
+    """The fast path is the default (QT_FAST_PATH=0 / set_fast_path(False)
+    selects the exact kernel); each test starts and ends with it enabled."""
     Q().set_fast_path(True)
     yield
-    Q().set_fast_path(False)
+    Q().set_fast_path(True)
 
 
 def _counts(plan, M, first=0, total=None, fast=True):
