@@ -131,6 +131,36 @@ QT_API qt_status qt_estimate(int32_t estimator, const qt_chain* chain, const qt_
                              uint64_t samples, int32_t engine, uint64_t seed, int32_t devices,
                              uint64_t* visits, uint64_t* joint, double* pi, double* phases_ms);
 
+/* ---- estimate -> price on the device (no pi round trip) --------------------
+ * The reference's pricers read the tree in place through a non-owning pointer
+ * (bdp.hpp:20-23, run_pipeline pipeline.hpp:190-215). qt_estimate_device runs
+ * qt_estimate but keeps joint / visits / pi in device memory (on the caller's
+ * current device) behind an opaque handle; qt_dtree_stopping / qt_dtree_swing
+ * are solve_stopping / solve_swing (same contract, same bits as qt_bdp_*) on
+ * it, with phi and the outputs in host memory. At config 4 this skips the
+ * 2.9 GB pi download and re-upload. */
+typedef struct qt_dtree qt_dtree;
+QT_API qt_status qt_estimate_device(int32_t estimator, const qt_chain* chain,
+                                    const qt_grids* grids, uint64_t samples, int32_t engine,
+                                    uint64_t seed, int32_t devices, qt_dtree** tree,
+                                    double* phases_ms);
+QT_API qt_status qt_dtree_destroy(qt_dtree* tree);
+/* n, dim, M, device and (when sizes_cap >= n + 1) sizes[0..n]; all nullable */
+QT_API qt_status qt_dtree_info(const qt_dtree* tree, int32_t* layers, int32_t* dim,
+                               uint64_t* samples, uint64_t* sizes, uint64_t sizes_cap,
+                               int32_t* device);
+/* the device buffers themselves (owned by the handle; valid until destroy) */
+QT_API qt_status qt_dtree_device_arrays(const qt_dtree* tree, const uint64_t** visits,
+                                        const uint64_t** joint, const double** pi);
+/* copy any of visits / joint / pi (nullable) to host arrays */
+QT_API qt_status qt_dtree_download(const qt_dtree* tree, uint64_t* visits, uint64_t* joint,
+                                   double* pi);
+QT_API qt_status qt_dtree_stopping(const qt_dtree* tree, const double* phi, double* value,
+                                   uint8_t* exercise, double* price);
+QT_API qt_status qt_dtree_swing(const qt_dtree* tree, const double* phi, int32_t qmin,
+                                int32_t qmax, double* price, double* value_all,
+                                uint8_t* take_all);
+
 /* Parity mode: the caller supplies every normal (path-major, n*nps per path
  * for Alg I/II; d+nps per sample, layer-major, for Alg III) instead of the
  * in-kernel stream. Counts are then bit-exact by construction. */

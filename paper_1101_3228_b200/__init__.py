@@ -10,6 +10,7 @@ from .qtree import (  # noqa: F401
     StoppingResult, SwingResult, TwoFactorChain, TwoFactorParams, accumulate_paths,
     ar1_coefficients, base_grid, build_brownian_grids, build_gbm_grids, build_ou_grids,
     build_two_factor_grids, estimate, estimate_alg1, estimate_alg2, estimate_alg3,
+    DeviceTree, estimate_device,
     cond_expectation, estimate_with_normals, layout, nearest, path_normals, solve_stopping,
     solve_swing,
     swing_window, tabulate, uniforms)

@@ -39,6 +39,16 @@ _SIGS = {
     "qt_chain_coefficients": [C.c_int32, C.POINTER(QtModelParams), _f64p, _f64p],
     "qt_estimate": [C.c_int32, C.POINTER(QtChain), C.POINTER(QtGrids), C.c_uint64, C.c_int32,
                     C.c_uint64, C.c_int32, _u64p, _u64p, _f64p, _f64p],
+    "qt_estimate_device": [C.c_int32, C.POINTER(QtChain), C.POINTER(QtGrids), C.c_uint64,
+                           C.c_int32, C.c_uint64, C.c_int32, C.POINTER(C.c_void_p), _f64p],
+    "qt_dtree_destroy": [C.c_void_p],
+    "qt_dtree_info": [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                      C.POINTER(C.c_uint64), _u64p, C.c_uint64, C.POINTER(C.c_int32)],
+    "qt_dtree_device_arrays": [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                               C.POINTER(C.c_void_p)],
+    "qt_dtree_download": [C.c_void_p, _u64p, _u64p, _f64p],
+    "qt_dtree_stopping": [C.c_void_p, _f64p, _f64p, _u8p, _f64p],
+    "qt_dtree_swing": [C.c_void_p, _f64p, C.c_int32, C.c_int32, _f64p, _f64p, _u8p],
     "qt_estimate_normals": [C.c_int32, C.POINTER(QtChain), C.POINTER(QtGrids), C.c_uint64,
                             _f64p, _u64p, _u64p, _f64p],
     "qt_accumulate_paths": [C.POINTER(QtChain), C.POINTER(QtGrids), C.c_int32, C.c_uint64,

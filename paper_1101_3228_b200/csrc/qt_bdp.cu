@@ -216,24 +216,36 @@ qt_status bdp_guarded(F&& f) {
   }
 }
 
+// The tree on the device: visits and pi either uploaded from host arrays
+// (owned) or borrowed from the caller's device buffers (the estimate -> price
+// path of qt_dtree_*: no pi round trip), plus the CSR of pi and phi.
 struct TreeOnDevice {
   int n;
   std::vector<uint64_t> sizes, voff, poff;
-  DevBuf<uint64_t> visits;
-  DevBuf<double> pi, phi;
+  DevBuf<uint64_t> visits_own;
+  DevBuf<double> pi_own, phi;
+  const uint64_t* visits = nullptr;
+  const double* pi = nullptr;
   Csr csr;
-  TreeOnDevice(int layers, const uint64_t* sz, const uint64_t* h_visits, const double* h_pi,
-               const double* h_phi)
+  TreeOnDevice(int layers, const uint64_t* sz, const uint64_t* vis, const double* pi_in,
+               const double* h_phi, bool device_arrays)
       : n(layers), sizes(sz, sz + layers + 1), voff(layers + 2, 0), poff(layers + 1, 0) {
     for (int k = 0; k <= n; ++k) voff[k + 1] = voff[k] + sizes[k];
     for (int t = 0; t < n; ++t) poff[t + 1] = poff[t] + sizes[t] * sizes[t + 1];
-    visits.alloc(voff[n + 1]);
-    pi.alloc(poff[n]);
+    if (device_arrays) {
+      visits = vis;
+      pi = pi_in;
+    } else {
+      visits_own.alloc(voff[n + 1]);
+      pi_own.alloc(poff[n]);
+      BDP_CUDA(cudaMemcpy(visits_own.p, vis, voff[n + 1] * 8, cudaMemcpyHostToDevice));
+      BDP_CUDA(qt::staged_copy(pi_own.p, pi_in, poff[n] * 8, true, 0));  // GBs for d >= 2 trees
+      visits = visits_own.p;
+      pi = pi_own.p;
+    }
     phi.alloc(voff[n + 1]);
-    BDP_CUDA(cudaMemcpy(visits.p, h_visits, voff[n + 1] * 8, cudaMemcpyHostToDevice));
-    BDP_CUDA(qt::staged_copy(pi.p, h_pi, poff[n] * 8, true, 0));  // GBs for d >= 2 trees
     BDP_CUDA(cudaMemcpy(phi.p, h_phi, voff[n + 1] * 8, cudaMemcpyHostToDevice));
-    build_csr(n, sizes, pi.p, poff, csr);
+    build_csr(n, sizes, pi, poff, csr);
   }
   const uint64_t* rowptr(int t) const { return csr.rowptr.p + csr.rp_off[t]; }
 };
@@ -257,10 +269,14 @@ void check_tree_args(int layers, const uint64_t* sizes, const uint64_t* visits, 
 
 extern "C" {
 
-QT_API qt_status qt_bdp_stopping(int32_t layers, const uint64_t* sizes, const uint64_t* visits,
-                                 const double* pi, const double* phi, double* value,
-                                 uint8_t* exercise, double* price) {
-  return bdp_guarded([&] {
+}  // extern "C"
+
+namespace {
+
+void stopping_impl(int32_t layers, const uint64_t* sizes, const uint64_t* visits, const double* pi,
+                   const double* phi, double* value, uint8_t* exercise, double* price,
+                   bool device_arrays) {
+  {
     check_tree_args(layers, sizes, visits, pi, phi);
     if (!price) bdp_raise(QT_ERR_INVALID_ARGUMENT, "solve_stopping: null output");
     uint64_t nodes = 0;
@@ -268,7 +284,7 @@ QT_API qt_status qt_bdp_stopping(int32_t layers, const uint64_t* sizes, const ui
     for (uint64_t i = 0; i < nodes; ++i)
       if (!std::isfinite(phi[i])) bdp_raise(QT_ERR_NUMERIC, "solve_stopping: non-finite payoff");
     check_device();
-    TreeOnDevice t(layers, sizes, visits, pi, phi);
+    TreeOnDevice t(layers, sizes, visits, pi, phi, device_arrays);
     const int n = layers;
     DevBuf<double> v(t.voff[n + 1]);
     DevBuf<uint8_t> ex(t.voff[n + 1]);
@@ -280,7 +296,7 @@ QT_API qt_status qt_bdp_stopping(int32_t layers, const uint64_t* sizes, const ui
     for (int k = n - 1; k >= 0; --k) {
       const uint64_t rows = sizes[k];
       k_stop_layer<<<static_cast<uint32_t>((rows + 127) / 128), 128>>>(
-          rows, t.rowptr(k), t.csr.colidx.p, t.csr.val.p, t.visits.p + t.voff[k],
+          rows, t.rowptr(k), t.csr.colidx.p, t.csr.val.p, t.visits + t.voff[k],
           t.phi.p + t.voff[k], v.p + t.voff[k + 1], v.p + t.voff[k], ex.p + t.voff[k]);
       qt::note_launches(1);
     }
@@ -288,13 +304,13 @@ QT_API qt_status qt_bdp_stopping(int32_t layers, const uint64_t* sizes, const ui
     BDP_CUDA(cudaMemcpy(price, v.p, 8, cudaMemcpyDeviceToHost));
     if (value) BDP_CUDA(qt::staged_copy(value, v.p, t.voff[n + 1] * 8, false, 0));
     if (exercise) BDP_CUDA(qt::staged_copy(exercise, ex.p, t.voff[n + 1], false, 0));
-  });
+  }
 }
 
-QT_API qt_status qt_bdp_swing(int32_t layers, const uint64_t* sizes, const uint64_t* visits,
-                              const double* pi, const double* phi, int32_t qmin, int32_t qmax,
-                              double* price, double* value_all, uint8_t* take_all) {
-  return bdp_guarded([&] {
+void swing_impl(int32_t layers, const uint64_t* sizes, const uint64_t* visits, const double* pi,
+                const double* phi, int32_t qmin, int32_t qmax, double* price, double* value_all,
+                uint8_t* take_all, bool device_arrays) {
+  {
     check_tree_args(layers, sizes, visits, pi, phi);
     const int n = layers;
     if (qmin < 0 || qmin > qmax) bdp_raise(QT_ERR_CONFIG, "swing: need 0 <= q_min <= q_max");
@@ -310,7 +326,7 @@ QT_API qt_status qt_bdp_swing(int32_t layers, const uint64_t* sizes, const uint6
           if (!std::isfinite(phi[o])) bdp_raise(QT_ERR_NUMERIC, "solve_swing: non-finite payoff");
     }
     check_device();
-    TreeOnDevice t(n, sizes, visits, pi, phi);
+    TreeOnDevice t(n, sizes, visits, pi, phi, device_arrays);
     std::vector<int> lo(n + 1), cnt(n + 1);
     std::vector<uint64_t> soff(n + 2, 0);
     for (int k = 0; k <= n; ++k) {
@@ -330,7 +346,7 @@ QT_API qt_status qt_bdp_swing(int32_t layers, const uint64_t* sizes, const uint6
       const uint64_t tc = rows * static_cast<uint64_t>(cnt[k + 1]);
       k_swing_cont<<<static_cast<uint32_t>((tc + 127) / 128), 128>>>(
           rows, sizes[k + 1], cnt[k + 1], t.rowptr(k), t.csr.colidx.p, t.csr.val.p,
-          t.visits.p + t.voff[k], P.p + soff[k + 1], cont.p);
+          t.visits + t.voff[k], P.p + soff[k + 1], cont.p);
       const uint64_t td = rows * static_cast<uint64_t>(cnt[k]);
       k_swing_decide<<<static_cast<uint32_t>((td + 127) / 128), 128>>>(
           rows, lo[k], cnt[k], lo[k + 1], n, k, qmin, qmax, t.phi.p + t.voff[k], cont.p,
@@ -341,8 +357,51 @@ QT_API qt_status qt_bdp_swing(int32_t layers, const uint64_t* sizes, const uint6
     BDP_CUDA(cudaMemcpy(price, P.p, 8, cudaMemcpyDeviceToHost));
     if (value_all) BDP_CUDA(qt::staged_copy(value_all, P.p, soff[n + 1] * 8, false, 0));
     if (take_all && soff[n]) BDP_CUDA(qt::staged_copy(take_all, take.p, soff[n], false, 0));
+  }
+}
+
+}  // namespace
+
+namespace qt {
+// estimate -> price on the device (qt_capi.cu's qt_dtree_*): visits / pi are
+// device arrays of the current device, phi and the outputs host arrays.
+void bdp_stopping_device(int32_t layers, const uint64_t* sizes, const uint64_t* d_visits,
+                         const double* d_pi, const double* phi, double* value, uint8_t* exercise,
+                         double* price) {
+  try {
+    stopping_impl(layers, sizes, d_visits, d_pi, phi, value, exercise, price, true);
+  } catch (const BdpFail& e) {
+    throw BdpError{e.code, e.msg};
+  }
+}
+void bdp_swing_device(int32_t layers, const uint64_t* sizes, const uint64_t* d_visits,
+                      const double* d_pi, const double* phi, int32_t qmin, int32_t qmax,
+                      double* price, double* value_all, uint8_t* take_all) {
+  try {
+    swing_impl(layers, sizes, d_visits, d_pi, phi, qmin, qmax, price, value_all, take_all, true);
+  } catch (const BdpFail& e) {
+    throw BdpError{e.code, e.msg};
+  }
+}
+}  // namespace qt
+
+extern "C" {
+
+QT_API qt_status qt_bdp_stopping(int32_t layers, const uint64_t* sizes, const uint64_t* visits,
+                                 const double* pi, const double* phi, double* value,
+                                 uint8_t* exercise, double* price) {
+  return bdp_guarded(
+      [&] { stopping_impl(layers, sizes, visits, pi, phi, value, exercise, price, false); });
+}
+
+QT_API qt_status qt_bdp_swing(int32_t layers, const uint64_t* sizes, const uint64_t* visits,
+                              const double* pi, const double* phi, int32_t qmin, int32_t qmax,
+                              double* price, double* value_all, uint8_t* take_all) {
+  return bdp_guarded([&] {
+    swing_impl(layers, sizes, visits, pi, phi, qmin, qmax, price, value_all, take_all, false);
   });
 }
+
 
 QT_API qt_status qt_bdp_cond_expectation(uint64_t rows, uint64_t cols, const uint64_t* row_visits,
                                          const double* pi, const double* f, double* out) {
@@ -354,12 +413,12 @@ QT_API qt_status qt_bdp_cond_expectation(uint64_t rows, uint64_t cols, const uin
     std::vector<double> no_phi(rows + cols, 0.0);
     std::vector<uint64_t> vis(rows + cols, 0);  // layer-1 visits are never read
     std::copy(row_visits, row_visits + rows, vis.begin());
-    TreeOnDevice t(1, sz, vis.data(), pi, no_phi.data());
+    TreeOnDevice t(1, sz, vis.data(), pi, no_phi.data(), false);
     DevBuf<double> df(cols), dout(rows);
     BDP_CUDA(cudaMemcpy(df.p, f, cols * 8, cudaMemcpyHostToDevice));
     // one stored slice, unvisited rows -> quiet NaN (bdp.hpp:45-48)
     k_swing_cont<<<static_cast<uint32_t>((rows + 127) / 128), 128>>>(
-        rows, cols, 1, t.rowptr(0), t.csr.colidx.p, t.csr.val.p, t.visits.p, df.p, dout.p);
+        rows, cols, 1, t.rowptr(0), t.csr.colidx.p, t.csr.val.p, t.visits, df.p, dout.p);
     qt::note_launches(1);
     BDP_CUDA(cudaGetLastError());
     BDP_CUDA(cudaMemcpy(out, dout.p, rows * 8, cudaMemcpyDeviceToHost));

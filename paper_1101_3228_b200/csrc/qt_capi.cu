@@ -1352,11 +1352,47 @@ void d2h_pinned(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   QT_CUDA(qt::staged_copy(dst, src, bytes, false, st));
 }
 
+}  // namespace
+
+// An estimated tree kept on the device (qt_estimate_device): counts, visits
+// and pi in the layouts of qt_estimate, on `device`; the pricers read them in
+// place (bdp.hpp:20-23 keeps a non-owning tree pointer the same way).
+struct qt_dtree {
+  int device = 0;
+  int layers = 0;
+  int dim = 0;
+  uint64_t samples = 0;
+  std::vector<uint64_t> sizes;
+  uint64_t nvis = 0, njoint = 0;
+  uint64_t* d_visits = nullptr;
+  uint64_t* d_joint = nullptr;
+  double* d_pi = nullptr;
+  ~qt_dtree() {
+    qt::DeviceRestore keep_device;
+    cudaSetDevice(device);
+    cudaFree(d_visits);
+    cudaFree(d_joint);
+    cudaFree(d_pi);
+  }
+};
+
+namespace {
+
+template <class F>
+void with_bdp_errors(F&& f) {
+  try {
+    f();
+  } catch (const qt::BdpError& e) {
+    raise(static_cast<qt_status>(e.code), e.msg);
+  }
+}
+
 // Shared body of qt_estimate / qt_estimate_normals / qt_accumulate_paths.
 void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_t samples,
                   int engine, uint64_t seed, int devices, const double* h_normals,
                   uint64_t win_first, uint64_t win_count, uint64_t win_total, bool accumulate,
-                  uint64_t* visits, uint64_t* joint, double* pi, double* phases) {
+                  uint64_t* visits, uint64_t* joint, double* pi, double* phases,
+                  qt_dtree** keep = nullptr) {
   const auto t0 = std::chrono::steady_clock::now();
   if (alg < QT_ALG_I || alg > QT_ALG_III)
     raise(QT_ERR_INVALID_ARGUMENT, "estimate: unknown estimator kind");
@@ -1434,7 +1470,7 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
       QT_CUDA(cudaEventRecord(ev[4 * g + 1], streams[g]));
     }
     Prefault prefault;  // host output pages, mapped while the counts run
-    if (!accumulate) {
+    if (!accumulate && !keep) {
       prefault.add(visits, plans[0]->nvis * 8);
       prefault.add(joint, plans[0]->njoint * 8);
       prefault.add(pi, plans[0]->njoint * 8);
@@ -1489,12 +1525,28 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
     plan_finalize(p0, alg, M_for_visits, dj[0], d_vis, d_pi, streams[0]);
     QT_CUDA(cudaEventRecord(ev[3], streams[0]));
     std::vector<uint64_t> hv, hj;
-    if (accumulate) {
+    if (keep) {  // the tree stays on the device: the handle takes the plan's result buffers
+      auto t = std::make_unique<qt_dtree>();
+      t->device = base;
+      t->layers = n;
+      t->dim = grids->dim;
+      t->samples = samples;
+      t->sizes.assign(grids->sizes, grids->sizes + n + 1);
+      t->nvis = p0->nvis;
+      t->njoint = p0->njoint;
+      t->d_joint = dj[0];
+      t->d_visits = d_vis;
+      t->d_pi = d_pi;
+      p0->d_ojoint = nullptr;
+      p0->d_ovis = nullptr;
+      p0->d_opi = nullptr;
+      *keep = t.release();
+    } else if (accumulate) {
       hv.resize(p0->nvis);
       hj.resize(p0->njoint);
       QT_CUDA(cudaMemcpyAsync(hv.data(), d_vis, p0->nvis * 8, cudaMemcpyDeviceToHost, streams[0]));
       QT_CUDA(cudaMemcpyAsync(hj.data(), dj[0], p0->njoint * 8, cudaMemcpyDeviceToHost, streams[0]));
-    } else {
+    } else if (!keep) {
       prefault.join();
       d2h_pinned(visits, d_vis, p0->nvis * 8, streams[0]);
       d2h_pinned(joint, dj[0], p0->njoint * 8, streams[0]);
@@ -1704,6 +1756,84 @@ QT_API qt_status qt_estimate(int32_t estimator, const qt_chain* chain, const qt_
     source_of(engine, false);
     run_estimate(estimator, chain, grids, samples, engine, seed, devices, nullptr, 0, 0, 0, false,
                  visits, joint, pi, phases_ms);
+  });
+}
+
+// ---- estimate -> price on the device ----------------------------------------
+QT_API qt_status qt_estimate_device(int32_t estimator, const qt_chain* chain,
+                                    const qt_grids* grids, uint64_t samples, int32_t engine,
+                                    uint64_t seed, int32_t devices, qt_dtree** tree,
+                                    double* phases_ms) {
+  return guarded([&] {
+    if (!tree) raise(QT_ERR_INVALID_ARGUMENT, "estimate: null output");
+    *tree = nullptr;
+    source_of(engine, false);
+    run_estimate(estimator, chain, grids, samples, engine, seed, devices, nullptr, 0, 0, 0, false,
+                 nullptr, nullptr, nullptr, phases_ms, tree);
+  });
+}
+
+QT_API qt_status qt_dtree_destroy(qt_dtree* tree) {
+  return guarded([&] { delete tree; });
+}
+
+QT_API qt_status qt_dtree_info(const qt_dtree* tree, int32_t* layers, int32_t* dim,
+                               uint64_t* samples, uint64_t* sizes, uint64_t sizes_cap,
+                               int32_t* device) {
+  return guarded([&] {
+    if (!tree) raise(QT_ERR_INVALID_ARGUMENT, "dtree: null tree");
+    if (layers) *layers = tree->layers;
+    if (dim) *dim = tree->dim;
+    if (samples) *samples = tree->samples;
+    if (device) *device = tree->device;
+    if (sizes && sizes_cap >= tree->sizes.size())
+      std::copy(tree->sizes.begin(), tree->sizes.end(), sizes);
+  });
+}
+
+QT_API qt_status qt_dtree_device_arrays(const qt_dtree* tree, const uint64_t** visits,
+                                        const uint64_t** joint, const double** pi) {
+  return guarded([&] {
+    if (!tree) raise(QT_ERR_INVALID_ARGUMENT, "dtree: null tree");
+    if (visits) *visits = tree->d_visits;
+    if (joint) *joint = tree->d_joint;
+    if (pi) *pi = tree->d_pi;
+  });
+}
+
+QT_API qt_status qt_dtree_download(const qt_dtree* tree, uint64_t* visits, uint64_t* joint,
+                                   double* pi) {
+  return guarded([&] {
+    if (!tree) raise(QT_ERR_INVALID_ARGUMENT, "dtree: null tree");
+    QT_CUDA(cudaSetDevice(tree->device));
+    if (visits) QT_CUDA(qt::staged_copy(visits, tree->d_visits, tree->nvis * 8, false, 0));
+    if (joint) QT_CUDA(qt::staged_copy(joint, tree->d_joint, tree->njoint * 8, false, 0));
+    if (pi) QT_CUDA(qt::staged_copy(pi, tree->d_pi, tree->njoint * 8, false, 0));
+  });
+}
+
+QT_API qt_status qt_dtree_stopping(const qt_dtree* tree, const double* phi, double* value,
+                                   uint8_t* exercise, double* price) {
+  return guarded([&] {
+    if (!tree) raise(QT_ERR_INVALID_ARGUMENT, "solve_stopping: incomplete problem");
+    QT_CUDA(cudaSetDevice(tree->device));
+    with_bdp_errors([&] {
+      qt::bdp_stopping_device(tree->layers, tree->sizes.data(), tree->d_visits, tree->d_pi, phi,
+                              value, exercise, price);
+    });
+  });
+}
+
+QT_API qt_status qt_dtree_swing(const qt_dtree* tree, const double* phi, int32_t qmin,
+                                int32_t qmax, double* price, double* value_all,
+                                uint8_t* take_all) {
+  return guarded([&] {
+    if (!tree) raise(QT_ERR_INVALID_ARGUMENT, "solve_swing: incomplete problem");
+    QT_CUDA(cudaSetDevice(tree->device));
+    with_bdp_errors([&] {
+      qt::bdp_swing_device(tree->layers, tree->sizes.data(), tree->d_visits, tree->d_pi, phi, qmin,
+                           qmax, price, value_all, take_all);
+    });
   });
 }
 

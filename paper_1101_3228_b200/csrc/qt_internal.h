@@ -178,6 +178,20 @@ cudaError_t launch_paths_x(int kind, bool resident, int P, const PathArgs& a, ui
 // layer t (sorted-cell counts of k_paths_x -> the reference's original indices);
 // fin = the finalize table (rows, cols, joff, voff_row, voff_col; 5 x n), orig
 // indexed by voff.
+// estimate -> price without the pi round trip (qt_bdp.cu): visits / pi are
+// device arrays on the current device; phi and the outputs are host arrays.
+// Failures throw BdpError {qt_status code, message}.
+struct BdpError {
+  int code;
+  std::string msg;
+};
+void bdp_stopping_device(int32_t layers, const uint64_t* sizes, const uint64_t* d_visits,
+                         const double* d_pi, const double* phi, double* value, uint8_t* exercise,
+                         double* price);
+void bdp_swing_device(int32_t layers, const uint64_t* sizes, const uint64_t* d_visits,
+                      const double* d_pi, const double* phi, int32_t qmin, int32_t qmax,
+                      double* price, double* value_all, uint8_t* take_all);
+
 cudaError_t launch_permute_add(const unsigned long long* sjoint, unsigned long long* joint,
                                const uint64_t* fin, const uint32_t* orig, uint32_t n,
                                uint64_t max_elems, cudaStream_t st);

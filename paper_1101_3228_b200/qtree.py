@@ -21,6 +21,7 @@ from __future__ import annotations
 import ctypes as C
 import dataclasses
 import enum
+import functools
 import math
 import os
 from dataclasses import dataclass, field
@@ -329,6 +330,85 @@ def _estimate(kind: int, chain: _Chain, grids: Sequence[QuantGrid], paths: int,
             opt.phases.normalize_ms, opt.phases.total_ms = (float(x) for x in ph)
     x0 = QuantGrid(chain.dim(), np.zeros(chain.dim()))
     return QuantTree([x0] + list(grids), gp.sizes, visits, joint, pi, paths)
+
+
+class DeviceTree:
+    """An estimated tree kept in device memory (qt_estimate_device): the
+    counts, visits and pi stay on the GPU and solve_stopping / solve_swing read
+    them in place, the way the reference's pricers hold a non-owning tree
+    pointer (bdp.hpp:20-23, run_pipeline pipeline.hpp:190-215). No pi round
+    trip: at config 4 that is 2.9 GB each way. download() gives the host
+    QuantTree; close() (or the context manager) frees the device memory."""
+
+    def __init__(self, handle: int, grids: list, sizes: np.ndarray, samples: int):
+        self._h = C.c_void_p(handle)
+        self.grids, self.sizes, self.samples = grids, sizes, samples
+
+    def layers(self) -> int:
+        return len(self.sizes) - 1
+
+    def layer_size(self, k: int) -> int:
+        return int(self.sizes[k])
+
+    def handle(self) -> C.c_void_p:
+        if not self._h:
+            raise ValueError("DeviceTree: already closed")
+        return self._h
+
+    def device_arrays(self) -> tuple[int, int, int]:
+        """Raw device pointers (visits, joint, pi), owned by this tree."""
+        v, j, p = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _check(L.lib().qt_dtree_device_arrays(self.handle(), C.byref(v), C.byref(j), C.byref(p)),
+               "dtree")
+        return v.value, j.value, p.value
+
+    def download(self) -> QuantTree:
+        nvis, njoint = layout(self.sizes)
+        visits = np.zeros(nvis, np.uint64)
+        joint = np.zeros(njoint, np.uint64)
+        pi = np.zeros(njoint, np.float64)
+        _check(L.lib().qt_dtree_download(self.handle(), _u(visits), _u(joint), _f(pi)), "dtree")
+        return QuantTree(self.grids, self.sizes, visits, joint, pi, self.samples)
+
+    def close(self) -> None:
+        if self._h:
+            L.lib().qt_dtree_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
+
+
+def estimate_device(kind, chain, grids, paths, opt=None) -> DeviceTree:
+    """estimate() with the result kept on the GPU (see DeviceTree)."""
+    opt = opt or EstimateOptions()
+    if int(kind) not in (0, 1, 2):
+        raise ValueError("estimate: unknown estimator kind")
+    if int(kind) in (1, 2) and opt.workers < 1:
+        raise ValueError(f"estimate_alg{int(kind) + 1}: workers must be >= 1")
+    if paths <= 0:
+        raise ValueError("estimate: need at least one path")
+    gp = _GridPack(chain, grids)
+    ph = np.zeros(5, np.float64)
+    ch = chain.c()
+    h = C.c_void_p()
+    _check(L.lib().qt_estimate_device(int(kind), C.byref(ch), C.byref(gp.s), int(paths),
+                                      int(opt.engine), int(opt.seed), int(opt.devices),
+                                      C.byref(h), _f(ph)), "estimate")
+    if opt.phases is not None:
+        opt.phases.simulate_ms, opt.phases.nn_ms, opt.phases.merge_ms, \
+            opt.phases.normalize_ms, opt.phases.total_ms = (float(x) for x in ph)
+    x0 = QuantGrid(chain.dim(), np.zeros(chain.dim()))
+    return DeviceTree(h.value, [x0] + list(grids), gp.sizes, int(paths))
 
 
 def estimate_alg1(chain, grids, paths, opt=None) -> QuantTree:
@@ -651,9 +731,13 @@ def solve_stopping(tree: QuantTree, payoff) -> StoppingResult:
     value = np.zeros(phi.size, np.float64)
     ex = np.zeros(phi.size, np.uint8)
     price = C.c_double()
-    _check(L.lib().qt_bdp_stopping(n, _u(tree.sizes), _u(tree.flat_visits), _f(tree.flat_pi),
-                                   _f(phi), _f(value), ex.ctypes.data_as(C.POINTER(C.c_uint8)),
-                                   C.byref(price)), "solve_stopping")
+    exp = ex.ctypes.data_as(C.POINTER(C.c_uint8))
+    if isinstance(tree, DeviceTree):  # in place on the device
+        rc = L.lib().qt_dtree_stopping(tree.handle(), _f(phi), _f(value), exp, C.byref(price))
+    else:
+        rc = L.lib().qt_bdp_stopping(n, _u(tree.sizes), _u(tree.flat_visits), _f(tree.flat_pi),
+                                     _f(phi), _f(value), exp, C.byref(price))
+    _check(rc, "solve_stopping")
     vs, es, o = [], [], 0
     for k in range(n + 1):
         s = tree.layer_size(k)
@@ -680,10 +764,14 @@ def solve_swing(tree: QuantTree, payoff, q_min: int, q_max: int) -> SwingResult:
     vals = np.zeros(max(total, 1), np.float64)
     takes = np.zeros(max(total, 1), np.uint8)
     price = C.c_double()
-    _check(L.lib().qt_bdp_swing(n, _u(tree.sizes), _u(tree.flat_visits), _f(tree.flat_pi),
-                                _f(phi), int(q_min), int(q_max), C.byref(price), _f(vals),
-                                takes.ctypes.data_as(C.POINTER(C.c_uint8))),
-           "solve_swing")
+    tkp = takes.ctypes.data_as(C.POINTER(C.c_uint8))
+    if isinstance(tree, DeviceTree):  # in place on the device
+        rc = L.lib().qt_dtree_swing(tree.handle(), _f(phi), int(q_min), int(q_max),
+                                    C.byref(price), _f(vals), tkp)
+    else:
+        rc = L.lib().qt_bdp_swing(n, _u(tree.sizes), _u(tree.flat_visits), _f(tree.flat_pi),
+                                  _f(phi), int(q_min), int(q_max), C.byref(price), _f(vals), tkp)
+    _check(rc, "solve_swing")
     value, take, o = [], [], 0
     for k in range(n + 1):
         s = cnt[k] * tree.layer_size(k)
@@ -714,9 +802,8 @@ def cond_expectation(tree: QuantTree, k: int, f) -> np.ndarray:
 
 # ---------------------------------------------------------------------------
 # grid inputs: the reference's per-layer mappings (pipeline.hpp:27-77) of the
-# standard-normal Lloyd base quantizers shipped in data/base_grids.npz
+# standard-normal Lloyd base quantizers, built on the GPU
 # ---------------------------------------------------------------------------
-_DATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "base_grids.npz")
 
 
 @dataclass
@@ -744,15 +831,21 @@ def lloyd_build(dim: int, n_points: int, iterations: int = 40, samples_per_iter:
     return LloydResult(QuantGrid(dim, out), dist[:iterations])
 
 
-def base_grid(grid_size: int, dim: int) -> np.ndarray:
-    """The standard-normal base quantizer of the grid builders: the reference's
-    own lloyd_build output where shipped (bit-identical, data/base_grids.npz),
-    else built on the GPU by lloyd_build (normals <= 1 ulp from glibc)."""
-    key = f"n{grid_size}_d{dim}"
-    with np.load(_DATA) as z:
-        if key in z:
-            return np.array(z[key])
-    return np.asarray(lloyd_build(dim, grid_size).grid.data(), np.float64)
+@functools.lru_cache(maxsize=16)
+def _base_grid(grid_size: int, dim: int, seed: int) -> np.ndarray:
+    g = np.asarray(lloyd_build(dim, grid_size, seed=seed).grid.data(), np.float64)
+    g.setflags(write=False)
+    return g
+
+
+def base_grid(grid_size: int, dim: int, seed: int = 12345) -> np.ndarray:
+    """The standard-normal base quantizer of the grid builders
+    (lloyd_build(GaussianSampler{dim}, N, dim, 40, max(20000, 200 N), g),
+    pipeline.hpp:27-77), built on the GPU. Bit-identical to the reference's:
+    the device Box-Muller restates glibc's log/sincos, the projection is exact
+    and every cell mean is summed in sample order (tests/test_lloyd.py against
+    the reference's own grids, tests/golden/base_grids.npz). Cached per process."""
+    return np.array(_base_grid(int(grid_size), int(dim), int(seed)))
 
 
 def _cholesky2_marginal(p: TwoFactorParams, t: float):

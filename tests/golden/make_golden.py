@@ -10,11 +10,11 @@ writes small .npz fixtures that travel with the repo:
                    C2-shape path-window hashes at M = 1e9
   pricing.npz      stopping / swing value tables on random row-stochastic trees
 
-It also writes paper_1101_3228_b200/data/base_grids.npz: the standard-normal
-Lloyd base quantizers the reference's grid builders map per layer
-(pipeline.hpp:27-77). Those are INPUT DATA for the CUDA path (grid
-construction is out of scope), produced by the reference's
-own lloyd_build with its default seed convention.
+It also writes tests/golden/base_grids.npz: the standard-normal Lloyd base
+quantizers the reference's grid builders map per layer (pipeline.hpp:27-77),
+produced by the reference's own lloyd_build with its default seed convention.
+The product builds them on the GPU (qt_lloyd_build); tests/test_lloyd.py
+requires the two to be bit-identical.
 
 Usage: python tests/golden/make_golden.py [--skip-c5]
 """
@@ -34,7 +34,7 @@ from pyoracle import (  # noqa: E402
     ChainSpec, Oracle, PAYOFF_PUT, PAYOFF_SWING)
 
 OUT = os.path.join(ROOT, "tests", "golden")
-DATA = os.path.join(ROOT, "paper_1101_3228_b200", "data")
+DATA = os.path.join(ROOT, "tests", "golden")
 
 
 def sha(a: np.ndarray) -> str:
@@ -85,7 +85,7 @@ def main() -> None:
         st[f"{tag}_window_joint"] = j
     np.savez_compressed(os.path.join(OUT, "small_trees.npz"), **st)
 
-    # ---- base grids (product input data) --------------------------------------
+    # ---- base grids (fixture: the GPU Lloyd must reproduce them bit for bit) ----
     bases = {}
     for tag, dim, N in (("n100_d1", 1, 100), ("n500_d1", 1, 500), ("n200_d1", 1, 200),
                         ("n1000_d2", 2, 1000)):
