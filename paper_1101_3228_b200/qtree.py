@@ -551,6 +551,12 @@ def bench_nn(n: int, queries: int, seed: int = 12345) -> tuple[int, float]:
     return sink.value, ms.value
 
 
+def plan_cache_clear() -> None:
+    """Free the device plans qt_estimate keeps for repeated calls on the same
+    inputs (tables, scratch and result buffers)."""
+    _check(L.lib().qt_plan_cache_clear(), "plan_cache_clear")
+
+
 def set_fast_path(enabled: bool) -> None:
     """Select the fast 1-D path (FP32 Box-Muller + certified cells + exact
     replay; identical counts) or the exact FP64 kernel for every path."""

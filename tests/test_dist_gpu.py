@@ -64,3 +64,36 @@ def test_two_rank_estimate_equals_single_process(gpu, tmp_path, kind):
     assert np.array_equal(got["joint"], t.flat_joint)
     assert np.array_equal(got["visits"], t.flat_visits)
     assert np.array_equal(got["pi"], t.flat_pi)
+
+
+def test_multi_device_one_call_equals_single_device(gpu):
+    """qt_estimate(devices=G) (estimate.hpp:163-207's worker merge across the
+    GPUs of one process: shards [M g/G, M (g+1)/G), one grouped NCCL
+    all-reduce) equals devices=1 bit for bit, and the caller's current
+    device is left as it was. Needs two visible GPUs (the gpurun box has
+    one: then only the single-device half and the error path run)."""
+    import torch
+    from paper_1101_3228_b200 import qtree as q
+    ch = q.BrownianChain1d(12)
+    grids = q.build_brownian_grids(ch, 120)
+    one = q.estimate_alg2(ch, grids, 200001)
+    visible = torch.cuda.device_count()
+    if visible < 2:
+        with pytest.raises(ValueError, match="devices"):
+            q.estimate_alg2(ch, grids, 1000, q.EstimateOptions(devices=2))
+        assert torch.cuda.current_device() == 0
+        pytest.skip(f"devices=2 needs two GPUs; this box has {visible} (error path checked)")
+    for G in sorted({2, min(visible, 4), visible}):
+        many = q.estimate_alg2(ch, grids, 200001, q.EstimateOptions(devices=G))
+        assert np.array_equal(many.flat_joint, one.flat_joint), G
+        assert np.array_equal(many.flat_visits, one.flat_visits), G
+        assert np.array_equal(many.flat_pi.view(np.uint64), one.flat_pi.view(np.uint64)), G
+        assert torch.cuda.current_device() == 0
+    # from another base device: devices [1, 2) of the process
+    torch.cuda.set_device(1)
+    try:
+        t = q.estimate_alg2(ch, grids, 200001)
+        assert np.array_equal(t.flat_joint, one.flat_joint)
+        assert torch.cuda.current_device() == 1
+    finally:
+        torch.cuda.set_device(0)
