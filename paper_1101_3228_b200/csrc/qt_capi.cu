@@ -59,6 +59,12 @@ bool scan_enabled() {
   return !(e && e[0] == '0');
 }
 
+// d >= 2 cell-list projection: enabled unless QT_NN=scan (then the FP32 scan)
+bool cell_enabled() {
+  const char* e = std::getenv("QT_NN");
+  return !(e && std::strcmp(e, "scan") == 0);
+}
+
 bool fast_enabled() {
   int v = g_fast.load();
   if (v < 0) {
@@ -522,6 +528,52 @@ std::vector<uint8_t> build_fast_table(int kind, const std::vector<double>& t,
 // One layer's table (layout in qt_layout.h). header.cold_off is patched by
 // the caller once the cold block's position is known.
 // FP32 scan table of one d >= 2 layer (ScanHdr + paired FP32 points), qt_layout.h
+// Bucket geometry of one d >= 2 layer's cell-list index (CellHdr,
+// qt_layout.h): the box of the points plus a 10 % margin, per N^(1/d)
+// buckets per axis (measured on B200: per = 6 for d = 2 (C4: 1.90e10
+// transitions/s; 4: 1.72e10, 1.5: 1.15e10), 5 for d = 3 (C5: 4.86e9; 4: 4.31e9,
+// 1.2: 8.4e8)). The lists themselves are built on the device
+// (qt::build_cell_lists).
+qt::CellHdr cell_geometry(int dim, uint64_t N, const double* pts) {
+  qt::CellHdr h{};
+  for (int c = 0; c < 3; ++c) {
+    h.g[c] = 1;
+    h.w[c] = 1.0;
+  }
+  if (dim < 2 || dim > 3 || N < 2 || N > 65535) return h;  // ok = 0: full scan
+  double mn[3] = {0, 0, 0}, mx[3] = {0, 0, 0};
+  for (int c = 0; c < dim; ++c) {
+    mn[c] = std::numeric_limits<double>::infinity();
+    mx[c] = -mn[c];
+    for (uint64_t i = 0; i < N; ++i) {
+      const double v = pts[i * dim + c];
+      if (!std::isfinite(v) || std::fabs(v) > 1e100) return h;
+      mn[c] = std::min(mn[c], v);
+      mx[c] = std::max(mx[c], v);
+    }
+  }
+  double per = dim == 2 ? 6.0 : 5.0;
+  if (const char* e = std::getenv(dim == 2 ? "QT_CELL_G2" : "QT_CELL_G3")) per = std::atof(e);
+  const uint32_t gax = static_cast<uint32_t>(
+      std::min(dim == 2 ? 1024.0 : 96.0, std::max(1.0, std::round(per * std::pow(double(N), 1.0 / dim)))));
+  for (int c = 0; c < dim; ++c) {
+    const double span = mx[c] - mn[c];
+    const double pad = span > 0.0 ? 0.1 * span : 0.5;
+    h.lo[c] = mn[c] - pad;
+    const double hi = mx[c] + pad;
+    h.g[c] = span > 0.0 ? gax : 1;
+    h.w[c] = (hi - h.lo[c]) / h.g[c];
+    h.inv_w[c] = h.g[c] / (hi - h.lo[c]);
+    // bucket corners lo + c w must resolve far below the 1e-6 w inflation
+    if (!(h.w[c] > 1e-9 * (std::fabs(h.lo[c]) + std::fabs(hi)))) {
+      h.ok = 0;
+      return h;
+    }
+  }
+  h.ok = 1;
+  return h;
+}
+
 std::vector<uint8_t> build_scan_table(int dim, uint64_t N, const double* pts, const double* step,
                                       uint64_t joff, uint64_t exact_off) {
   qt::ScanHdr h{};
@@ -721,6 +773,9 @@ struct qt_plan {
   qt::AmbEntry* d_amb = nullptr;
   unsigned long long* d_stats = nullptr;
   uint8_t* d_stables = nullptr;  // FP32 scan tables (d >= 2), concatenated
+  qt::CellHdr* d_chdr = nullptr;  // cell-list index (d >= 2, qt_cell.cu): headers [n],
+  uint32_t* d_cstart = nullptr;   // bucket starts over all layers, and
+  uint16_t* d_clist = nullptr;    // the candidate lists
   uint32_t* d_stab_off = nullptr;
   uint32_t* d_stab_bytes = nullptr;
   uint32_t max_stab = 0, total_stab = 0;
@@ -761,6 +816,9 @@ struct qt_plan {
     cudaFree(d_stats);
     cudaFree(d_ftables);
     cudaFree(d_stables);
+    cudaFree(d_chdr);
+    cudaFree(d_cstart);
+    cudaFree(d_clist);
     cudaFree(d_stab_off);
     cudaFree(d_stab_bytes);
     cudaFree(d_ftab_off);
@@ -894,6 +952,19 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
     }
     p->total_stab = static_cast<uint32_t>(stables.size());
   }
+  // cell-list geometry (d >= 2); the lists are built on the device below
+  std::vector<qt::CellHdr> chdr;
+  if (p->dim >= 2 && cell_enabled()) {
+    const double* sp = grids->points;
+    uint64_t off = 0;
+    for (int k = 1; k <= n; ++k) {
+      qt::CellHdr h = cell_geometry(p->dim, p->sizes[k], sp);
+      h.start_off = off;
+      off += static_cast<uint64_t>(h.g[0]) * h.g[1] * h.g[2];
+      chdr.push_back(h);
+      sp += p->sizes[k] * p->dim;
+    }
+  }
   QT_CUDA(cudaSetDevice(device));
   QT_CUDA(cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, device));
   QT_CUDA(cudaMalloc(&p->d_tables, p->host_tables.size()));
@@ -927,6 +998,18 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
   QT_CUDA(cudaMemcpy(p->d_tab_off, p->tab_off.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
   QT_CUDA(cudaMemcpy(p->d_tab_bytes, p->tab_bytes.data(), n * sizeof(uint32_t),
                      cudaMemcpyHostToDevice));
+  if (!chdr.empty()) {
+    std::vector<uint64_t> pts_off(n);
+    for (int k = 1; k <= n; ++k) {
+      const qt::LayerTable& lt =
+          *reinterpret_cast<const qt::LayerTable*>(p->host_tables.data() + p->tab_off[k - 1]);
+      pts_off[k - 1] = p->tab_off[k - 1] + lt.off_rec;
+    }
+    uint64_t total = 0;
+    QT_CUDA(qt::build_cell_lists(p->dim, n, chdr.data(), p->sizes.data() + 1, p->d_tables,
+                                 pts_off.data(), &p->d_chdr, &p->d_cstart, &p->d_clist, &total));
+    g_launches.fetch_add(2ull * n + 1);
+  }
   std::vector<uint64_t> fin(5 * n);
   for (int t = 0; t < n; ++t) {
     fin[t] = p->sizes[t];
@@ -962,7 +1045,8 @@ std::vector<uint8_t> plan_key(const qt_chain* chain, const qt_grids* grids, int 
     const uint8_t* b = static_cast<const uint8_t*>(p);
     k.insert(k.end(), b, b + n);
   };
-  const int32_t hdr[5] = {chain->kind, chain->layers, grids->dim, device, fast_enabled() ? 1 : 0};
+  const int32_t hdr[6] = {chain->kind, chain->layers, grids->dim, device, fast_enabled() ? 1 : 0,
+                          cell_enabled() ? 1 : 0};
   put(hdr, sizeof hdr);
   const size_t n = static_cast<size_t>(chain->layers);
   put(chain->step, 6 * n * sizeof(double));
@@ -1132,6 +1216,22 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       g_launches.fetch_add(2);
       return 2;
     }
+    if (p->d_chdr && cell_enabled()) {  // d >= 2: exact cell-list search (qt_cell.cu)
+      int P = 2;
+      if (const char* e = std::getenv("QT_CELL_P")) P = std::atoi(e) == 1 ? 1 : 2;
+      const int cbps = qt::paths_cell_blocks_per_sm(p->kind, src, P);
+      uint64_t cblocks = static_cast<uint64_t>(p->sm_count) * cbps;
+      const uint64_t per_block = 256ull * P;  // kCellThreads
+      const uint64_t cneed = (count + per_block - 1) / per_block;
+      if (cneed < cblocks) cblocks = cneed;
+      const uint64_t T = cblocks * per_block;
+      qt::CellArgs ca{a, p->d_chdr, p->d_cstart, p->d_clist};
+      ca.p.q = count / T;
+      ca.p.rem = count % T;
+      QT_CUDA(qt::launch_paths_cell(p->kind, src, P, ca, static_cast<uint32_t>(cblocks), st));
+      g_launches.fetch_add(1);
+      return 1;
+    }
     if (p->d_stables && scan_enabled()) {  // d >= 2: FP32 scan + exact FP64 decision
       // queries per thread: d = 2 keeps two CTAs per SM at P = 2; d = 3 is one
       // CTA per SM anyway (64 KB tables), where P = 4 gives the ILP
@@ -1213,6 +1313,9 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
                                      p->max_elems, st));
       g_launches.fetch_add(1);
       extra = 1;
+    } else if (p->d_chdr && cell_enabled()) {  // d >= 2: exact cell-list search
+      qt::Alg3CellArgs ca{a, p->d_chdr, p->d_cstart, p->d_clist};
+      QT_CUDA(qt::launch_alg3_cell(p->kind, src, ca, static_cast<uint32_t>(slices), st));
     } else if (p->d_stables && scan_enabled() && 2ull * p->max_stab <= 200u * 1024u) {
       qt::Alg3ScanArgs sa{a, p->d_stables, p->d_stab_off, p->d_stab_bytes, p->max_stab};
       QT_CUDA(qt::launch_alg3_scan(p->kind, src, sa, static_cast<uint32_t>(slices),

@@ -129,6 +129,27 @@ struct Alg3Args {
   const uint8_t* xtables;  // k_alg3_x: threshold-pair tables (see PathArgs::xtables)
 };
 
+// d >= 2 cell-list path kernels (qt_cell.cu): exact tables (FP64 points) and
+// the cell-list tables, both read from global memory (L2-resident)
+struct CellArgs {
+  PathArgs p;
+  const CellHdr* chdr;        // [n] layer k's header at index k-1
+  const uint32_t* cstart;     // bucket list starts, all layers (+ a final end)
+  const uint16_t* clist;      // candidate point indices, ascending per bucket
+};
+struct Alg3CellArgs {
+  Alg3Args a;
+  const CellHdr* chdr;
+  const uint32_t* cstart;
+  const uint16_t* clist;
+};
+// Builds the cell lists of n layers on the current device (synchronous):
+// hdr[n] (host) geometry with start_off set, npts[n] = N_k, the FP64 points of
+// layer k at tables + pts_off[k-1]. Allocates *d_hdr, *d_start, *d_list.
+cudaError_t build_cell_lists(int dim, int n, const CellHdr* hdr, const uint64_t* npts,
+                             const uint8_t* tables, const uint64_t* pts_off, CellHdr** d_hdr,
+                             uint32_t** d_start, uint16_t** d_list, uint64_t* total);
+
 struct FinalizeArgs {
   const uint64_t* rows;      // [n] N_{t}
   const uint64_t* cols;      // [n] N_{t+1}
@@ -198,6 +219,11 @@ cudaError_t launch_permute_add(const unsigned long long* sjoint, unsigned long l
 cudaError_t launch_paths_scan(int kind, int src, bool resident, int P, const ScanArgs& a,
                               uint32_t blocks, size_t smem, cudaStream_t st);
 int paths_scan_blocks_per_sm(int kind, int src, bool resident, int P, size_t smem);
+cudaError_t launch_paths_cell(int kind, int src, int P, const CellArgs& a, uint32_t blocks,
+                              cudaStream_t st);
+int paths_cell_blocks_per_sm(int kind, int src, int P);
+cudaError_t launch_alg3_cell(int kind, int src, const Alg3CellArgs& a, uint32_t slices,
+                             cudaStream_t st);
 cudaError_t launch_alg3_scan(int kind, int src, const Alg3ScanArgs& a, uint32_t slices,
                              size_t smem, cudaStream_t st);
 cudaError_t launch_nearest_scan(int dim, const uint8_t* stable, uint32_t sbytes,

@@ -130,6 +130,28 @@ inline uint32_t fbucket_host(double x, double gc, double bk_a, double bk_b, uint
 // ---------------------------------------------------------------------------
 constexpr uint32_t kScanChunkPairs = 16;  // 32 points per chunk
 
+// ---------------------------------------------------------------------------
+// Cell-list index of one d >= 2 layer (qt_cell.cu), in global memory: a
+// CellHdr per layer, one start[] array over all layers' buckets (u32, the
+// list position of each bucket, plus a final end) and one list[] of u16 point
+// indices (ascending per bucket). The bounding box [lo, lo + g w) of the
+// layer's points (plus a margin) is cut into g[0] x g[1] (x g[2]) buckets;
+// bucket b lists every point that can be the reference's nearest point
+// (nn.hpp:18-46, FP64 d2, strict <) -- or tie with it -- for some query in b,
+// so the exact argmin over the list equals the brute-force one. Queries
+// outside the box (or non-finite) take the exact full scan. The lists are
+// built on the device (k_cell_count / k_cell_fill).
+// ---------------------------------------------------------------------------
+struct alignas(16) CellHdr {
+  double lo[3];        // box origin per axis
+  double w[3];         // bucket width per axis
+  double inv_w[3];     // buckets per unit length per axis (the query's bucket map)
+  uint64_t start_off;  // index of this layer's bucket 0 in start[]
+  uint32_t g[3];       // buckets per axis (1 on unused axes)
+  uint32_t ok;         // 0: no bucket grid (degenerate layer): always the full scan
+};
+static_assert(sizeof(CellHdr) == 96, "CellHdr is 96 bytes");
+
 struct alignas(16) ScanHdr {
   double step[6];     // chain coefficients of transition k-1 -> k
   uint64_t joff;      // element offset of joint[k-1]

@@ -1,10 +1,13 @@
-"""K2 for d >= 2: the FP32 brute-force scan with an exact FP64 decision
-(k_paths_scan, qt_scan.cu) must give exactly the reference's cells.
+"""K2 for d >= 2: both fast projections must give exactly the reference's cells
+-- the default exact cell-list search (k_paths_cell / k_alg3_cell, qt_cell.cu)
+and the FP32 brute-force scan with an exact FP64 decision (k_paths_scan /
+k_alg3_scan, qt_scan.cu; QT_NN=scan).
 
-Checked against the exact FP64 kernel (QT_SCAN=0 selects it) on the config-4
-and config-5 chains and grids, on adversarial grids (exact ties, near-ties
-closer than the FP32 error bound, coordinates too large for FP32, far-away
-queries), and against the CPU oracle on windows of the config chains."""
+Both are checked against the exact FP64 brute-force kernel (QT_NN=scan +
+QT_SCAN=0) on the config-4 and config-5 chains and grids, on adversarial grids
+(exact ties, near-ties closer than the FP32 error bound, coordinates too large
+for FP32, far-away queries, degenerate and tiny grids), and against the CPU
+oracle on windows of the config chains."""
 from __future__ import annotations
 
 import numpy as np
@@ -20,10 +23,22 @@ def Q():
     return qtree
 
 
-def _counts(monkeypatch, chain, grids, M, first=0, total=None, scan=True, engine=1):
+MODES = ("cell", "scan", "exact")
+
+
+def _mode(monkeypatch, mode):
+    if mode == "cell":
+        monkeypatch.delenv("QT_NN", raising=False)
+        monkeypatch.setenv("QT_SCAN", "1")
+    else:
+        monkeypatch.setenv("QT_NN", "scan")
+        monkeypatch.setenv("QT_SCAN", "1" if mode == "scan" else "0")
+
+
+def _counts(monkeypatch, chain, grids, M, first=0, total=None, mode="cell", engine=1):
     import torch
     from paper_1101_3228_b200.device import Plan
-    monkeypatch.setenv("QT_SCAN", "1" if scan else "0")
+    _mode(monkeypatch, mode)
     plan = Plan(chain, grids, 0)
     joint = plan.zeros_joint()
     plan.count(1, engine, 12345, first, M, total or M, joint)
@@ -37,9 +52,8 @@ def test_scan_equals_exact_c4(gpu, monkeypatch):
     tf = q.TwoFactorChain(q.TwoFactorParams())
     g4 = q.build_two_factor_grids(tf, 1000)
     for first in (0, 31415926):
-        a = _counts(monkeypatch, tf, g4, 20000, first, 10**8, True)
-        b = _counts(monkeypatch, tf, g4, 20000, first, 10**8, False)
-        assert np.array_equal(a, b), first
+        a, b, c = (_counts(monkeypatch, tf, g4, 20000, first, 10**8, m) for m in MODES)
+        assert np.array_equal(a, c) and np.array_equal(b, c), first
         assert int(a[:1000].sum()) == 20000
 
 
@@ -47,9 +61,8 @@ def test_scan_equals_exact_c5(gpu, monkeypatch):
     q = Q()
     ch = q.GbmChain3d(20, 1.0, (0.0, 0.0, 0.0))
     g5 = q.build_gbm_grids(ch, 4000)
-    a = _counts(monkeypatch, ch, g5, 20000, 777, 4 * 10**9, True)
-    b = _counts(monkeypatch, ch, g5, 20000, 777, 4 * 10**9, False)
-    assert np.array_equal(a, b)
+    a, b, c = (_counts(monkeypatch, ch, g5, 20000, 777, 4 * 10**9, m) for m in MODES)
+    assert np.array_equal(a, c) and np.array_equal(b, c)
 
 
 @pytest.mark.parametrize("engine", [0, 2])
@@ -57,11 +70,12 @@ def test_scan_other_engines(gpu, monkeypatch, engine):
     q = Q()
     tf = q.TwoFactorChain(q.TwoFactorParams(steps=30))
     g = q.build_two_factor_grids(tf, 1000)
-    assert np.array_equal(_counts(monkeypatch, tf, g, 30000, 0, None, True, engine),
-                          _counts(monkeypatch, tf, g, 30000, 0, None, False, engine))
+    a, b, c = (_counts(monkeypatch, tf, g, 30000, 0, None, m, engine) for m in MODES)
+    assert np.array_equal(a, c) and np.array_equal(b, c)
 
 
-@pytest.mark.parametrize("case", ["ties", "near_ties", "huge", "far", "tiny_grid"])
+@pytest.mark.parametrize("case", ["ties", "near_ties", "huge", "far", "tiny_grid", "two_points",
+                                  "collinear", "near_duplicates", "cluster_and_outlier"])
 def test_scan_adversarial_grids(gpu, monkeypatch, case):
     q = Q()
     n = 8
@@ -79,12 +93,21 @@ def test_scan_adversarial_grids(gpu, monkeypatch, case):
             pts = rng.standard_normal(400) * 1e13
         elif case == "far":  # queries far outside a small cluster
             pts = rng.standard_normal(400) * 1e-3 + 5.0
-        else:  # fewer points than one chunk
+        elif case == "tiny_grid":  # fewer points than one chunk
             pts = rng.standard_normal(6)
+        elif case == "two_points":
+            pts = np.array([0.1, -0.2, -0.3, 0.4])
+        elif case == "collinear":  # zero span on one axis: one bucket across it
+            pts = np.stack([np.linspace(-1, 1, 50), np.full(50, 0.25)], axis=1).reshape(-1)
+        elif case == "near_duplicates":  # copies 1 ulp apart (exact copies are invalid grids)
+            base = rng.standard_normal((60, 2)) * 0.4
+            pts = np.concatenate([base, np.nextafter(base, np.inf)[::-1]]).reshape(-1)
+        else:  # a dense cluster and one far point: most buckets empty
+            pts = np.concatenate([rng.standard_normal((200, 2)) * 1e-2, [[3.0, -2.0]]]).reshape(-1)
         grids.append(q.QuantGrid(2, pts))
-    a = _counts(monkeypatch, tf, grids, 50000, 0, None, True)
-    b = _counts(monkeypatch, tf, grids, 50000, 0, None, False)
-    assert np.array_equal(a, b), case
+    a, b, c = (_counts(monkeypatch, tf, grids, 50000, 0, None, m) for m in MODES)
+    assert np.array_equal(a, c), ("cell", case)
+    assert np.array_equal(b, c), ("scan", case)
 
 
 def test_scan_c4_window_vs_oracle(gpu, oracle):
@@ -113,7 +136,8 @@ def test_scan_c5_window_vs_oracle(gpu, oracle):
 
 @pytest.mark.parametrize("kind,engine", [("tf", 1), ("tf", 2), ("gbm", 1), ("gbm", 0)])
 def test_alg3_scan_equals_exact(gpu, monkeypatch, kind, engine):
-    """Alg III (layer-parallel pairs) through k_alg3_scan vs the FP64 k_alg3."""
+    """Alg III (layer-parallel pairs) through k_alg3_cell and k_alg3_scan vs
+    the FP64 k_alg3."""
     import torch
     from paper_1101_3228_b200.device import Plan
     q = Q()
@@ -126,12 +150,12 @@ def test_alg3_scan_equals_exact(gpu, monkeypatch, kind, engine):
     M = 20000
     units = M * ch.layers()
     out = []
-    for scan in ("1", "0"):
-        monkeypatch.setenv("QT_SCAN", scan)
+    for mode in MODES:
+        _mode(monkeypatch, mode)
         plan = Plan(ch, grids, 0)
         joint = plan.zeros_joint()
         plan.count(2, engine, 4242, 0, units, units, joint)
         torch.cuda.synchronize()
         out.append(joint.cpu().numpy().copy())
         plan.close()
-    assert np.array_equal(out[0], out[1])
+    assert np.array_equal(out[0], out[2]) and np.array_equal(out[1], out[2])
