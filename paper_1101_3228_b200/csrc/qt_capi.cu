@@ -1217,7 +1217,8 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       return 2;
     }
     if (p->d_chdr && cell_enabled()) {  // d >= 2: exact cell-list search (qt_cell.cu)
-      int P = 2;
+      // paths per thread: 2 for d = 2 (C4 2.36e10 vs 2.17e10), 1 for d = 3 (C5 5.55e9 vs 4.43e9)
+      int P = p->dim == 3 ? 1 : 2;
       if (const char* e = std::getenv("QT_CELL_P")) P = std::atoi(e) == 1 ? 1 : 2;
       const int cbps = qt::paths_cell_blocks_per_sm(p->kind, src, P);
       uint64_t cblocks = static_cast<uint64_t>(p->sm_count) * cbps;

@@ -32,6 +32,9 @@
 namespace qt {
 
 constexpr int kCellThreads = 256;
+#ifndef QT_CELL_MINB  // resident CTAs per SM the register allocation must allow
+#define QT_CELL_MINB 3  // the kernel is load-latency bound: warps in flight pay (C4 +24 %)
+#endif
 
 // The reference's d2 of point idx (nn.hpp:25-45), FP64, read through the
 // read-only path.
@@ -235,7 +238,7 @@ cudaError_t build_cell_lists(int dim, int n, const CellHdr* hdr, const uint64_t*
 // Alg I / II: P paths per thread, every layer's tables from global memory.
 // Slot v = gid P + p owns a contiguous run of paths (one serial stream).
 template <int K, int SRC, int P>
-__global__ void __launch_bounds__(kCellThreads) k_paths_cell(const __grid_constant__ CellArgs f) {
+__global__ void __launch_bounds__(kCellThreads, QT_CELL_MINB) k_paths_cell(const __grid_constant__ CellArgs f) {
   using C = Chain<K>;
   constexpr int D = C::D;
   const PathArgs& a = f.p;

@@ -3,7 +3,8 @@
 #               the default bench command
 #   PART=traffic  DRAM bytes of the full-size C2 count launch (M = 1e9)
 #   PART=kx     ncu --set full of k_paths_x (C2 grids, 1e9 transitions)
-#   PART=c4     ncu --set full of k_paths_scan (C4, 3.65e8 transitions)
+#   PART=c4     ncu --set full of the d >= 2 path kernel (C4, 3.65e8 transitions)
+#   PART=c5     the same for C5 (8e6 transitions)
 #   PART=c3     ncu --set full of k_alg3_x (C3, 3.65e8 samples)
 # Outputs land in gpurun_out/$TAG_*; summaries go to profiles/.
 TAG=${TAG:-r01e}
@@ -24,8 +25,11 @@ kx)
   ncu --set full --clock-control none --import-source on -k regex:k_paths_x -c 1 -o $O/${TAG}_kx \
       python bench.py --paths 2e7 --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 1 > $O/${TAG}_ncu_kx.log 2>&1 ;;
 c4)
-  ncu --set full --clock-control none --import-source on -k regex:k_paths_scan -c 1 -o $O/${TAG}_scan_c4 \
+  ncu --set full --clock-control none --import-source on -k regex:"k_paths_(scan|cell)" -c 1 -o $O/${TAG}_c4 \
       python bench.py --config c4 --paths 1e6 --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 1 > $O/${TAG}_ncu_c4.log 2>&1 ;;
+c5)
+  ncu --set full --clock-control none --import-source on -k regex:"k_paths_(scan|cell)" -c 1 -o $O/${TAG}_c5 \
+      python bench.py --config c5 --paths 4e5 --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 1 > $O/${TAG}_ncu_c5.log 2>&1 ;;
 c3)
   ncu --set full --clock-control none --import-source on -k regex:k_alg3_x -c 1 -o $O/${TAG}_alg3x_c3 \
       python bench.py --config c3 --paths 1e6 --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 1 > $O/${TAG}_ncu_c3.log 2>&1 ;;
