@@ -479,8 +479,12 @@ def run_ours(args, rank, world, local_rank):
                          "uncertified paths replayed exactly with the glibc-exact FP64 "
                          "Box-Muller) + k_permute_add",
                    "ou": "k_alg3_x (layer-parallel pair sampler)" if est == 2 else "k_paths_x",
-                   "tf": "k_paths_scan (FP64 path + FP32 FFMA2 brute-force scan, exact decision)",
-                   "gbm": "k_paths_scan (FP64 path + FP32 FFMA2 brute-force scan, exact decision)"}[kind]
+                   "tf": "k_paths_cell (FP64 path + exact cell-list nearest-point search: "
+                         "FP64 reference d2 over the bucket's candidate list)",
+                   "gbm": "k_paths_cell (FP64 path + exact cell-list nearest-point search: "
+                          "FP64 reference d2 over the bucket's candidate list)"}[kind]
+    if kind in ("tf", "gbm") and os.environ.get("QT_NN") == "scan":
+        kernel_name = "k_paths_scan (FP64 path + FP32 FFMA2 brute-force scan, exact decision)"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
@@ -498,10 +502,13 @@ def run_ours(args, rank, world, local_rank):
                      "kernel": kernel_name,
                      "kernel_ms": t_kern, "peak_source": peak_src,
                      "algorithmic_bytes": "16 B per transition (u64 counter read-modify-write)",
-                     "binding_unit": ("d = 1: the count scatter's L2 atomic throughput (one "
-                                      "64-bit RED per transition; tools/red_probe.cu measures "
-                                      "1.5-1.9e11 REDs/s on this B200 for this access pattern, "
-                                      "profiles/r02_red_probe_*.txt); see DESIGN.md section 4")},
+                     "binding_unit": (
+                         "d = 1: the count scatter's L2 atomic throughput (one 64-bit RED per "
+                         "transition; tools/red_probe.cu measures 1.3-1.9e11 REDs/s on this B200 "
+                         "for such patterns, profiles/r02_red_probe_*.txt)" if kind in ("bm", "ou")
+                         else "d >= 2: load latency of the candidate-list gathers (ncu: "
+                              "long-scoreboard stalls ~58 %, profiles/r02_ncu_kernels.md)") +
+                         "; see DESIGN.md section 4"},
         "e2e": {"value": transitions / (t_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e, "steps": e2e_steps,
                 "plan": "cold: plan cache cleared before every call (tables built + uploaded)"},
@@ -523,7 +530,12 @@ def run_ours(args, rank, world, local_rank):
                                   "accumulate) so the step outlasts the 200 ms clock sampler")
     if price_line is not None:
         line["price"] = price_line
-    if kind in ("tf", "gbm"):  # FP32-bound configs: 3 d N flop per transition
+    if kind in ("tf", "gbm"):
+        # SURVEY 8(d) models d >= 2 as the brute-force scan, FP32-bound at 3 d N flop per
+        # transition. The default projection (cell lists) evaluates ~10-40 points, not N:
+        # this line states the brute-force-equivalent rate against that FP32 bound (a frac
+        # above 1 is work the cell lists do not need to do); the FP32 scan itself
+        # (QT_NN=scan) is measured against it in profiles/.
         fp32_peak, fp32_src = fp32_peak_tflops()
         flops = 3.0 * (2 if kind == "tf" else 3) * N * kern_units
         line["roofline_fp32"] = {"bound": "fp32", "achieved": flops / (t_kern / 1e3) / 1e12,
@@ -531,6 +543,9 @@ def run_ours(args, rank, world, local_rank):
                                  "frac": flops / (t_kern / 1e3) / 1e12 / fp32_peak,
                                  "algorithmic_flops": "3 d N per transition (brute-force "
                                                       "convention, PAPER.md:540-543)",
+                                 "meaning": ("brute-force-equivalent rate of the cell-list "
+                                             "search" if os.environ.get("QT_NN") != "scan"
+                                             else "FP32 scan"),
                                  "peak_source": fp32_src}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, args.ref_seconds, grids)
