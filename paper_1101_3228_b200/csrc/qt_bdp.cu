@@ -81,6 +81,22 @@ __device__ __forceinline__ double row_dot(const uint64_t* rowptr, const uint32_t
   return acc;
 }
 
+// The reference's dense row sum sum_j pi[i][j] f[j], j ascending (bdp.hpp:49-50),
+// for an f with non-finite entries: there 0 * inf = NaN terms matter, so the
+// CSR shortcut (skipping pi == 0) would differ. One thread per row.
+__global__ void k_row_dense(uint64_t rows, uint64_t cols, const double* pi, const uint64_t* visits,
+                            const double* f, double* out) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  if (visits[i] == 0) {
+    out[i] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  double acc = 0.0;
+  for (uint64_t j = 0; j < cols; ++j) acc = __dadd_rn(acc, __dmul_rn(pi[i * cols + j], f[j]));
+  out[i] = acc;
+}
+
 // V_k = max(phi_k, E V_{k+1}); unvisited rows absorb (bdp.hpp:79-93)
 __global__ void k_stop_layer(uint64_t rows, const uint64_t* rowptr, const uint32_t* colidx,
                              const double* val, const uint64_t* visits, const double* phi,
@@ -413,6 +429,21 @@ QT_API qt_status qt_bdp_cond_expectation(uint64_t rows, uint64_t cols, const uin
     std::vector<double> no_phi(rows + cols, 0.0);
     std::vector<uint64_t> vis(rows + cols, 0);  // layer-1 visits are never read
     std::copy(row_visits, row_visits + rows, vis.begin());
+    bool finite = true;
+    for (uint64_t j = 0; j < cols && finite; ++j) finite = std::isfinite(f[j]);
+    if (!finite) {  // the dense loop, exactly as the reference (0 * inf = NaN included)
+      DevBuf<double> dpi(rows * cols), df(cols), dout(rows);
+      DevBuf<uint64_t> dvis(rows);
+      BDP_CUDA(qt::staged_copy(dpi.p, pi, rows * cols * 8, true, 0));
+      BDP_CUDA(cudaMemcpy(df.p, f, cols * 8, cudaMemcpyHostToDevice));
+      BDP_CUDA(cudaMemcpy(dvis.p, row_visits, rows * 8, cudaMemcpyHostToDevice));
+      k_row_dense<<<static_cast<uint32_t>((rows + 127) / 128), 128>>>(rows, cols, dpi.p, dvis.p,
+                                                                       df.p, dout.p);
+      qt::note_launches(1);
+      BDP_CUDA(cudaGetLastError());
+      BDP_CUDA(cudaMemcpy(out, dout.p, rows * 8, cudaMemcpyDeviceToHost));
+      return;
+    }
     TreeOnDevice t(1, sz, vis.data(), pi, no_phi.data(), false);
     DevBuf<double> df(cols), dout(rows);
     BDP_CUDA(cudaMemcpy(df.p, f, cols * 8, cudaMemcpyHostToDevice));

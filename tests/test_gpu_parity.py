@@ -355,3 +355,40 @@ def test_swing_on_estimated_tree(gpu, oracle):
     sp = q.solve_swing(t, phi, 2, 6)
     rp = oracle.solve_swing(t.sizes, t.flat_visits, t.flat_pi, phi, 2, 6)
     assert sp.price == rp
+
+
+def test_cond_expectation_non_finite_f(gpu):
+    """cond_expectation (bdp.hpp:36-54) with inf / NaN in f: the reference's
+    dense loop multiplies every pi entry, so 0 * inf = NaN reaches rows whose
+    non-zero entries avoid the non-finite columns; the device must agree bit
+    for bit (a sequential Python-float loop is the reference's arithmetic)."""
+    q = Q()
+    rng = np.random.default_rng(7)
+    rows, cols = 9, 7
+    pi = rng.random((rows, cols)) * (rng.random((rows, cols)) < 0.5)
+    pi[2] = 0.0
+    pi[3, 4] = 0.3
+    vis = np.array([5, 3, 0, 7, 1, 2, 9, 4, 6], np.uint64)
+    flat_vis = np.concatenate([[1], vis, np.zeros(cols)]).astype(np.uint64)
+    flat_pi = np.concatenate([np.full(rows, 1.0 / rows), pi.reshape(-1)])
+    tree = q.QuantTree([q.QuantGrid(1, [0.0]), q.QuantGrid(1, np.arange(rows, dtype=float)),
+                        q.QuantGrid(1, np.arange(cols, dtype=float))],
+                       np.array([1, rows, cols], np.uint64), flat_vis,
+                       np.zeros(rows + rows * cols, np.uint64), flat_pi, 1)
+    for f in ([1.0, np.inf, 2.0, 3.0, 4.0, 5.0, 6.0], [1.0, 2.0, np.nan, 3.0, -np.inf, 5.0, 6.0],
+              [np.inf, -np.inf, 1.0, 1.0, 1.0, 1.0, 1.0], list(rng.standard_normal(cols))):
+        f = np.array(f)
+        got = q.cond_expectation(tree, 1, f)
+        want = []
+        for i in range(rows):
+            if vis[i] == 0:
+                want.append(float("nan"))
+                continue
+            acc = 0.0
+            for j in range(cols):
+                acc += float(pi[i, j]) * float(f[j])
+            want.append(acc)
+        want = np.array(want)
+        assert np.array_equal(np.isnan(got), np.isnan(want)), (f, got, want)
+        ok = ~np.isnan(want)
+        assert np.array_equal(got[ok].view(np.uint64), want[ok].view(np.uint64)), (f, got, want)
