@@ -240,6 +240,30 @@ QT_API qt_status qt_lloyd_build(int32_t dim, uint64_t n_points, int32_t iteratio
                                 uint64_t samples_per_iter, uint64_t stream_seed,
                                 const double* normals, uint64_t n_normals, double* centers,
                                 double* distortion);
+/* lloyd_build with GaussianSampler{dim} on the caller's MRG32k3a RngStream in
+ * block mode: state6 = {s1[0..2], s2[0..2]} (oldest first, mrg32k3a.hpp:17-20),
+ * *has_spare / *spare its cached Box-Muller mate (stream.hpp:97-103). On
+ * return the three hold the stream's state after the build, exactly where the
+ * reference's lloyd_build leaves g. samples_per_iter 0 is allowed (NaN
+ * distortions, centers unchanged, as the reference). */
+QT_API qt_status qt_lloyd_build_stream(int32_t dim, uint64_t n_points, int32_t iterations,
+                                       uint64_t samples_per_iter, uint64_t* state6,
+                                       int32_t* has_spare, double* spare, double* centers,
+                                       double* distortion);
+/* distortion (lloyd.hpp:30-48) with GaussianSampler{dim} on the caller's
+ * MRG32k3a stream (state as above, advanced on return). */
+QT_API qt_status qt_distortion_stream(int32_t dim, uint64_t n_points, const double* centers,
+                                      uint64_t samples, uint64_t* state6, int32_t* has_spare,
+                                      double* spare, double* mean, double* std_error);
+/* Any PointSampler: the caller draws the samples (M x dim, sample-major) on the
+ * host; one Lloyd iteration (lloyd.hpp:86-106: exact cells, per-cell means in
+ * sample order, empty cells kept) updates centers in place, and the distortion
+ * (lloyd.hpp:30-48) of a grid is measured on given samples. */
+QT_API qt_status qt_lloyd_iterate(int32_t dim, uint64_t n_points, double* centers, uint64_t M,
+                                  const double* X, double* distortion);
+QT_API qt_status qt_distortion_points(int32_t dim, uint64_t n_points, const double* centers,
+                                      uint64_t M, const double* X, double* mean,
+                                      double* std_error);
 
 /* ---- micro-benchmarks (qtree_main.cpp bench-rng / bench-nn) -------------- */
 /* estimate_pi_partitioned (monte_carlo.hpp:51-77): samples uniforms (a positive

@@ -180,6 +180,26 @@ Mat3 mat_pow_inv(Mat3 c, uint64_t e, uint64_t m) {
 }
 
 // MRG32k3a state <- (J^D)^-1 state: from the end of a path back to its start
+// state <- J^e state on the host (mrg32k3a_skip, mrg32k3a.hpp:124-146):
+// s[0..2] component 1, s[3..5] component 2, oldest first.
+void mrg_skip_host(uint64_t s[6], uint64_t e) {
+  static const std::vector<uint32_t> J = mrg_jump_table();
+  for (int b = 0; e != 0; ++b, e >>= 1) {
+    if (!(e & 1ull)) continue;
+    for (int c = 0; c < 2; ++c) {
+      const uint64_t m = c ? kM2 : kM1;
+      const uint32_t* M = J.data() + b * 18 + 9 * c;
+      uint64_t r[3];
+      for (int i = 0; i < 3; ++i) {
+        u128 acc = 0;
+        for (int j = 0; j < 3; ++j) acc += static_cast<u128>(M[3 * i + j]) * s[3 * c + j];
+        r[i] = static_cast<uint64_t>(acc % m);
+      }
+      for (int i = 0; i < 3; ++i) s[3 * c + i] = r[i];
+    }
+  }
+}
+
 void mrg_back_jump(uint64_t D, uint32_t out[18]) {
   const Mat3 c1{{{0, 1, 0}, {0, 0, 1}, {kM1 - 810728ull, 1403580ull, 0}}};
   const Mat3 c2{{{0, 1, 0}, {0, 0, 1}, {kM2 - 1370589ull, 0, 527612ull}}};
@@ -2055,11 +2075,28 @@ cudaError_t project_on_device(int dim, const GridTables& g, const uint8_t* d_blo
 // MRG32k3a stream seeded `stream_seed` (the pipeline passes seed ^ 0x9E3779B9,
 // pipeline.hpp:35,63). normals (nullable): the stream's normals supplied by the
 // caller (parity mode), at least as many as the build consumes.
-QT_API qt_status qt_lloyd_build(int32_t dim, uint64_t n_points, int32_t iterations,
-                                uint64_t samples_per_iter, uint64_t stream_seed,
-                                const double* normals, uint64_t n_normals, double* centers,
-                                double* distortion) {
-  return guarded([&] {
+}  // extern "C"
+
+namespace {
+
+// The serial normal stream of lloyd_build / distortion: an optional cached
+// Box-Muller mate of the caller's RngStream first (stream.hpp:97-103), then
+// the stream's own normals from `src` (pair p from uniforms 2p, 2p+1), or the
+// caller's normals (parity mode).
+struct NormalStream {
+  qt::SrcArgs src{};
+  bool lead = false;        // a cached mate precedes the device normals
+  double lead_value = 0.0;
+  const double* normals = nullptr;  // parity mode
+  uint64_t n_normals = 0;
+};
+
+// lloyd_build (lloyd.hpp:59-107) with the GaussianSampler; returns the number
+// of normals consumed from the stream.
+uint64_t lloyd_core(int32_t dim, uint64_t n_points, int32_t iterations, uint64_t samples_per_iter,
+                    const NormalStream& ns, double* centers, double* distortion) {
+  uint64_t used_total = 0;
+  {
     if (n_points == 0) raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: need at least one center");
     if (iterations < 0) raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: iterations must be >= 0");
     if (dim < 1 || dim > 3) raise(QT_ERR_NUMERIC, "lloyd_build: sampler dimension mismatch");
@@ -2071,9 +2108,9 @@ QT_API qt_status qt_lloyd_build(int32_t dim, uint64_t n_points, int32_t iteratio
     int avail = 0;
     if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
       raise(QT_ERR_DEVICE, "cuda: no CUDA device available (the build has no CPU path)");
-    const int dev0 = qt::current_device();  // the caller's device
     const uint64_t d = static_cast<uint64_t>(dim), N = n_points, M = samples_per_iter;
-    const qt::SrcArgs src = make_src(dev0, QT_ENGINE_MRG32K3A, stream_seed, 1, 1, nullptr, 0);
+    const double* normals = ns.normals;
+    const uint64_t n_normals = ns.n_normals;
     cudaStream_t st = nullptr;
     std::vector<void*> bufs;
     auto dalloc = [&](size_t bytes) {
@@ -2095,8 +2132,18 @@ QT_API qt_status qt_lloyd_build(int32_t dim, uint64_t n_points, int32_t iteratio
             raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: not enough normals supplied");
           QT_CUDA(cudaMemcpyAsync(dst_dev, normals + consumed, count * 8, cudaMemcpyHostToDevice, st));
         } else {
-          QT_CUDA(qt::launch_serial_normals(src, consumed, count, dst_dev, st));
-          g_launches.fetch_add(1);
+          uint64_t at = consumed, n = count;
+          double* dst = dst_dev;
+          if (ns.lead && at == 0 && n > 0) {  // the caller's cached mate comes first
+            QT_CUDA(cudaMemcpyAsync(dst, &ns.lead_value, 8, cudaMemcpyHostToDevice, st));
+            ++dst;
+            --n;
+            ++at;
+          }
+          if (n) {
+            QT_CUDA(qt::launch_serial_normals(ns.src, at - (ns.lead ? 1 : 0), n, dst, st));
+            g_launches.fetch_add(1);
+          }
         }
         consumed += count;
       };
@@ -2167,11 +2214,279 @@ QT_API qt_status qt_lloyd_build(int32_t dim, uint64_t n_points, int32_t iteratio
       }
       check_grid(dim, N, c.data(), 0);  // result.grid = QuantGrid(dim, centers)
       std::memcpy(centers, c.data(), N * d * 8);
+      QT_CUDA(cudaStreamSynchronize(st));
+      used_total = consumed;
     } catch (...) {
       cleanup();
       throw;
     }
     cleanup();
+  }
+  return used_total;
+}
+
+void lloyd_args(int32_t dim, uint64_t n_points, int32_t iterations, uint64_t samples_per_iter,
+                const double* centers) {
+  if (n_points == 0) raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: need at least one center");
+  if (iterations < 0) raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: iterations must be >= 0");
+  if (dim < 1 || dim > 3) raise(QT_ERR_NUMERIC, "lloyd_build: sampler dimension mismatch");
+  if (!centers) raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: null output");
+  if (samples_per_iter == 0 && iterations > 0)
+    raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: samples_per_iter must be >= 1");
+  if (samples_per_iter > 0x7fffffffull || n_points > 0x7fffffffull)
+    raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: batch too large");
+  int avail = 0;
+  if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+    raise(QT_ERR_DEVICE, "cuda: no CUDA device available (the build has no CPU path)");
+}
+
+// The caller's RngStream state (s1[3], s2[3], cached mate) -> NormalStream.
+NormalStream stream_of(const uint64_t* state6, int32_t has_spare, double spare) {
+  NormalStream ns;
+  ns.src = make_src(qt::current_device(), QT_ENGINE_MRG32K3A, 0, 1, 1, nullptr, 0);
+  for (int i = 0; i < 6; ++i) {
+    const uint64_t m = i < 3 ? kM1 : kM2;
+    if (state6[i] >= m) raise(QT_ERR_INVALID_ARGUMENT, "rng: MRG32k3a state word out of range");
+    ns.src.mrg_seed[i] = static_cast<uint32_t>(state6[i]);
+  }
+  ns.lead = has_spare != 0;
+  ns.lead_value = spare;
+  return ns;
+}
+
+// Leave the caller's stream where the reference's would be after `used`
+// normals: the device normals consumed D = used - lead advance the state by
+// 2 ceil(D / 2) uniforms, and an odd D leaves the last pair's mate cached.
+void advance_stream(const NormalStream& ns, uint64_t used, uint64_t* state6, int32_t* has_spare,
+                    double* spare) {
+  if (used == 0) return;
+  if (ns.lead && used == 1) {
+    *has_spare = 0;
+    return;
+  }
+  const uint64_t D = used - (ns.lead ? 1 : 0);
+  const uint64_t pairs = (D + 1) / 2;
+  if (D % 2 == 1) {  // the mate of pair D / 2 is normal D of the device stream
+    double* dn = nullptr;
+    QT_CUDA(cudaMalloc(&dn, 8));
+    cudaError_t e = qt::launch_serial_normals(ns.src, D, 1, dn, nullptr);
+    if (e == cudaSuccess) e = cudaMemcpy(spare, dn, 8, cudaMemcpyDeviceToHost);
+    cudaFree(dn);
+    QT_CUDA(e);
+    g_launches.fetch_add(1);
+    *has_spare = 1;
+  } else {
+    *has_spare = 0;
+  }
+  mrg_skip_host(state6, 2 * pairs);
+}
+
+}  // namespace
+
+extern "C" {
+
+QT_API qt_status qt_lloyd_build(int32_t dim, uint64_t n_points, int32_t iterations,
+                                uint64_t samples_per_iter, uint64_t stream_seed,
+                                const double* normals, uint64_t n_normals, double* centers,
+                                double* distortion) {
+  return guarded([&] {
+    lloyd_args(dim, n_points, iterations, samples_per_iter, centers);
+    NormalStream ns;
+    ns.src = make_src(qt::current_device(), QT_ENGINE_MRG32K3A, stream_seed, 1, 1, nullptr, 0);
+    ns.normals = normals;
+    ns.n_normals = n_normals;
+    lloyd_core(dim, n_points, iterations, samples_per_iter, ns, centers, distortion);
+  });
+}
+
+QT_API qt_status qt_lloyd_build_stream(int32_t dim, uint64_t n_points, int32_t iterations,
+                                       uint64_t samples_per_iter, uint64_t* state6,
+                                       int32_t* has_spare, double* spare, double* centers,
+                                       double* distortion) {
+  return guarded([&] {
+    // zero samples per iteration: the reference's iterations assign nothing, keep
+    // every center and record 0 / 0 (lloyd.hpp:97-105)
+    const bool empty = samples_per_iter == 0 && iterations > 0;
+    lloyd_args(dim, n_points, empty ? 0 : iterations, samples_per_iter, centers);
+    if (!state6 || !has_spare || !spare) raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: null stream");
+    const NormalStream ns = stream_of(state6, *has_spare, *spare);
+    const uint64_t used = lloyd_core(dim, n_points, empty ? 0 : iterations, samples_per_iter, ns,
+                                     centers, distortion);
+    if (empty && distortion) {
+      volatile double zero = 0.0;  // the reference's dist_sum / 0 (lloyd.hpp:97), same NaN bits
+      for (int it = 0; it < iterations; ++it) distortion[it] = zero / zero;
+    }
+    advance_stream(ns, used, state6, has_spare, spare);
+  });
+}
+
+// One iteration of lloyd_build (lloyd.hpp:86-106) on caller-drawn samples X
+// (M x dim, sample-major; any PointSampler): the snapshot's exact cells on the
+// device, per-cell sums in sample order (stable sort, one thread per cell),
+// empty cells keep their point; *distortion = the mean squared distance to the
+// old centers, summed in sample order.
+QT_API qt_status qt_lloyd_iterate(int32_t dim, uint64_t n_points, double* centers, uint64_t M,
+                                  const double* X, double* distortion) {
+  return guarded([&] {
+    if (dim < 1 || dim > 3 || n_points == 0 || !centers || !X || M == 0 || !distortion)
+      raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: bad iteration arguments");
+    if (M > 0x7fffffffull || n_points > 0x7fffffffull)
+      raise(QT_ERR_INVALID_ARGUMENT, "lloyd_build: batch too large");
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+      raise(QT_ERR_DEVICE, "cuda: no CUDA device available (the build has no CPU path)");
+    check_grid(dim, n_points, centers, 0);  // QuantGrid snapshot(dim, centers)
+    const uint64_t d = static_cast<uint64_t>(dim), N = n_points;
+    std::vector<void*> bufs;
+    auto dalloc = [&](size_t bytes) {
+      void* p = nullptr;
+      QT_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+      bufs.push_back(p);
+      return p;
+    };
+    try {
+      double* dX = static_cast<double*>(dalloc(M * d * 8));
+      double* dC = static_cast<double*>(dalloc(N * d * 8));
+      double* dd2 = static_cast<double*>(dalloc(M * 8));
+      auto* dcell = static_cast<unsigned long long*>(dalloc(M * 8));
+      auto* key = static_cast<uint32_t*>(dalloc(M * 4));
+      auto* idx = static_cast<uint32_t*>(dalloc(M * 4));
+      auto* key2 = static_cast<uint32_t*>(dalloc(M * 4));
+      auto* idx2 = static_cast<uint32_t*>(dalloc(M * 4));
+      auto* cnt = static_cast<uint32_t*>(dalloc(N * 4));
+      auto* offs = static_cast<uint32_t*>(dalloc(N * 4));
+      const size_t tmp_bytes = qt::lloyd_tmp_bytes(M, N);
+      void* tmp = dalloc(tmp_bytes);
+      const GridTables gt = grid_tables(dim, N, centers);
+      uint8_t* dT = static_cast<uint8_t*>(dalloc(gt.blob.size()));
+      QT_CUDA(cudaMemcpy(dT, gt.blob.data(), gt.blob.size(), cudaMemcpyHostToDevice));
+      QT_CUDA(qt::staged_copy(dX, X, M * d * 8, true, 0));
+      QT_CUDA(cudaMemcpy(dC, centers, N * d * 8, cudaMemcpyHostToDevice));
+      QT_CUDA(project_on_device(dim, gt, dT, dX, M, dcell, nullptr));
+      QT_CUDA(qt::launch_lloyd_update(dX, dcell, M, N, dim, dC, dd2, key, idx, key2, idx2, cnt, offs,
+                                      tmp, tmp_bytes, nullptr));
+      g_launches.fetch_add(5);
+      std::vector<double> hd2(M);
+      QT_CUDA(cudaMemcpy(hd2.data(), dd2, M * 8, cudaMemcpyDeviceToHost));
+      QT_CUDA(cudaMemcpy(centers, dC, N * d * 8, cudaMemcpyDeviceToHost));
+      double sum = 0.0;
+      for (uint64_t m = 0; m < M; ++m) sum += hd2[m];
+      *distortion = sum / static_cast<double>(M);
+    } catch (...) {
+      for (void* b : bufs) cudaFree(b);
+      throw;
+    }
+    for (void* b : bufs) cudaFree(b);
+  });
+}
+
+// distortion (lloyd.hpp:30-48) on caller-drawn samples X (M x dim): exact cells
+// on the device, sum and sum of squares in sample order on the host.
+QT_API qt_status qt_distortion_points(int32_t dim, uint64_t n_points, const double* centers,
+                                      uint64_t M, const double* X, double* mean,
+                                      double* std_error) {
+  return guarded([&] {
+    if (M == 0) raise(QT_ERR_INVALID_ARGUMENT, "distortion: samples must be >= 1");
+    if (dim < 1 || dim > 3 || n_points == 0 || !centers || !X || !mean || !std_error)
+      raise(QT_ERR_INVALID_ARGUMENT, "distortion: null argument");
+    std::vector<uint64_t> cell(M);
+    if (const qt_status rc = qt_nearest(dim, n_points, centers, M, X, cell.data()))
+      raise(rc, std::string(g_error));
+    const uint64_t d = static_cast<uint64_t>(dim);
+    double sum = 0.0, sum_sq = 0.0;
+    for (uint64_t m = 0; m < M; ++m) {
+      const double* x = X + m * d;
+      const double* c = centers + cell[m] * d;
+      double d2 = 0.0;  // squared_distance (grid.hpp:65-72)
+      for (uint64_t j = 0; j < d; ++j) {
+        volatile double t = x[j] - c[j];
+        volatile double tt = t * t;
+        d2 = d2 + tt;
+      }
+      sum += d2;
+      volatile double sq = d2 * d2;
+      sum_sq += sq;
+    }
+    const double mu = sum / static_cast<double>(M);
+    const double var = std::max(0.0, sum_sq / static_cast<double>(M) - mu * mu);
+    *mean = mu;
+    *std_error = std::sqrt(var / static_cast<double>(M));
+  });
+}
+
+// distortion (lloyd.hpp:30-48): E min_i |X - x_i|^2 over `samples` GaussianSampler
+// draws of the caller's stream; the cells by the exact projection, the sums in
+// sample order on the host (sum, sum of squares; as the reference).
+QT_API qt_status qt_distortion_stream(int32_t dim, uint64_t n_points, const double* centers,
+                                      uint64_t samples, uint64_t* state6, int32_t* has_spare,
+                                      double* spare, double* mean, double* std_error) {
+  return guarded([&] {
+    if (samples == 0) raise(QT_ERR_INVALID_ARGUMENT, "distortion: samples must be >= 1");
+    if (dim < 1 || dim > 3 || n_points == 0 || !centers)
+      raise(QT_ERR_NUMERIC, "distortion: sampler dimension mismatch");
+    if (!state6 || !has_spare || !spare || !mean || !std_error)
+      raise(QT_ERR_INVALID_ARGUMENT, "distortion: null argument");
+    if (samples > 0x7fffffffull) raise(QT_ERR_INVALID_ARGUMENT, "distortion: batch too large");
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+      raise(QT_ERR_DEVICE, "cuda: no CUDA device available (the build has no CPU path)");
+    check_grid(dim, n_points, centers, 0);
+    const NormalStream ns = stream_of(state6, *has_spare, *spare);
+    const uint64_t d = static_cast<uint64_t>(dim), total = samples * d;
+    double* dX = nullptr;
+    unsigned long long* dcell = nullptr;
+    uint8_t* dT = nullptr;
+    auto fin = [&] {
+      cudaFree(dX);
+      cudaFree(dcell);
+      cudaFree(dT);
+    };
+    try {
+      QT_CUDA(cudaMalloc(&dX, total * 8));
+      QT_CUDA(cudaMalloc(&dcell, samples * 8));
+      double* dst = dX;
+      uint64_t n = total;
+      if (ns.lead) {
+        QT_CUDA(cudaMemcpy(dst, &ns.lead_value, 8, cudaMemcpyHostToDevice));
+        ++dst;
+        --n;
+      }
+      if (n) {
+        QT_CUDA(qt::launch_serial_normals(ns.src, 0, n, dst, nullptr));
+        g_launches.fetch_add(1);
+      }
+      const GridTables gt = grid_tables(dim, n_points, centers);
+      QT_CUDA(cudaMalloc(&dT, gt.blob.size()));
+      QT_CUDA(cudaMemcpy(dT, gt.blob.data(), gt.blob.size(), cudaMemcpyHostToDevice));
+      QT_CUDA(project_on_device(dim, gt, dT, dX, samples, dcell, nullptr));
+      std::vector<double> X(total);
+      std::vector<unsigned long long> cell(samples);
+      QT_CUDA(cudaMemcpy(X.data(), dX, total * 8, cudaMemcpyDeviceToHost));
+      QT_CUDA(cudaMemcpy(cell.data(), dcell, samples * 8, cudaMemcpyDeviceToHost));
+      double sum = 0.0, sum_sq = 0.0;
+      for (uint64_t m = 0; m < samples; ++m) {
+        const double* x = X.data() + m * d;
+        const double* c = centers + cell[m] * d;
+        double d2 = 0.0;  // squared_distance (grid.hpp:65-72), coordinate order from 0.0
+        for (uint64_t j = 0; j < d; ++j) {
+          volatile double t = x[j] - c[j];  // volatile: no contraction
+          volatile double tt = t * t;
+          d2 = d2 + tt;
+        }
+        sum += d2;
+        volatile double sq = d2 * d2;
+        sum_sq += sq;
+      }
+      const double mu = sum / static_cast<double>(samples);
+      const double var = std::max(0.0, sum_sq / static_cast<double>(samples) - mu * mu);
+      *mean = mu;
+      *std_error = std::sqrt(var / static_cast<double>(samples));
+    } catch (...) {
+      fin();
+      throw;
+    }
+    fin();
+    advance_stream(ns, total, state6, has_spare, spare);
   });
 }
 

@@ -32,6 +32,7 @@ struct RefLib {
   decltype(&oq_solve_swing) swing = nullptr;
   decltype(&oq_solve_stopping) stopping = nullptr;
   decltype(&oq_payoff_table) payoff_table = nullptr;
+  decltype(&oq_build_grids) build_grids = nullptr;
   RefLib() {
     const char* p = std::getenv("QTREE_REF_LIB");
     void* h = dlopen(p ? p : "oracle/_ref/libqtree_ref.so", RTLD_NOW | RTLD_LOCAL);
@@ -44,6 +45,7 @@ struct RefLib {
     swing = reinterpret_cast<decltype(swing)>(dlsym(h, "oq_solve_swing"));
     stopping = reinterpret_cast<decltype(stopping)>(dlsym(h, "oq_solve_stopping"));
     payoff_table = reinterpret_cast<decltype(payoff_table)>(dlsym(h, "oq_payoff_table"));
+    build_grids = reinterpret_cast<decltype(build_grids)>(dlsym(h, "oq_build_grids"));
   }
 };
 
@@ -274,4 +276,73 @@ TEST_CASE("errors keep the reference's exception types", "[dropin]") {
   CHECK_THROWS_AS(pricer::solve_stopping(nan_payoff), NumericError);
   CHECK_THROWS_AS(pricer::cond_expectation(t, 3, std::vector<double>(2, 0.0)),
                   std::invalid_argument);
+}
+
+// ---- quant/lloyd.hpp drop-in (lloyd.hpp:30-107) ------------------------------
+
+TEST_CASE("pipeline.hpp grid builders on the drop-in Lloyd equal the reference's", "[dropin]") {
+  // build_brownian_grids / build_two_factor_grids call lloyd_build(GaussianSampler, ...)
+  // on an MRG32k3a block stream: the drop-in runs it on the device
+  model::TwoFactorParams p;
+  p.steps = 6;
+  for (int kind : {OQ_CHAIN_BROWNIAN1D, OQ_CHAIN_TWO_FACTOR}) {
+    std::vector<quant::QuantGrid> grids;
+    const std::size_t N = kind == OQ_CHAIN_BROWNIAN1D ? 150 : 120;
+    if (kind == OQ_CHAIN_BROWNIAN1D)
+      grids = build_brownian_grids(model::BrownianChain1d(p.steps), N, 777);
+    else
+      grids = build_two_factor_grids(model::ar1_coefficients(p), N, 777);
+    const oq_chain c = oq_of(kind, p);
+    std::vector<double> want(static_cast<std::size_t>(p.steps) * N * grids[0].dim());
+    REQUIRE(ref().build_grids(&c, N, 777, 0, 40, want.data()) == 0);
+    std::vector<double> got;
+    for (const auto& g : grids) got.insert(got.end(), g.data().begin(), g.data().end());
+    REQUIRE(got.size() == want.size());
+    for (std::size_t i = 0; i < got.size(); ++i) CHECK(got[i] == want[i]);
+  }
+}
+
+TEST_CASE("drop-in lloyd_build and distortion leave the stream where the reference does",
+          "[dropin]") {
+  // N = 7 centers of d = 3 and 2 x 5 samples consume 21 + 30 = 51 normals: an odd
+  // count, so the stream ends holding a cached Box-Muller mate
+  for (bool spare_first : {false, true}) {
+    auto g = rng::split_stream(rng::EngineKind::Mrg32k3a, 99, rng::StreamPartition{});
+    auto h = g;  // the reference's view: draw the same normals on the host
+    if (spare_first) {  // start with a cached mate
+      (void)g.next_gaussian();
+      (void)h.next_gaussian();
+    }
+    const auto res = quant::lloyd_build(quant::GaussianSampler{3}, 7, 3, 2, 5, g);
+    for (int k = 0; k < 51; ++k) (void)h.next_gaussian();
+    for (int k = 0; k < 5; ++k) CHECK(g.next_gaussian() == h.next_gaussian());
+    CHECK(res.distortion.size() == 2);
+    const auto e = quant::distortion(res.grid, quant::GaussianSampler{3}, 9, g);
+    for (int k = 0; k < 27; ++k) (void)h.next_gaussian();
+    CHECK(g.next_gaussian() == h.next_gaussian());
+    CHECK(e.samples == 9);
+  }
+}
+
+TEST_CASE("drop-in lloyd_build with a host sampler matches the device stream path", "[dropin]") {
+  // a sampler that is not GaussianSampler draws on the host; here it draws the same
+  // normals, so the grid and the distortions must equal the all-device build
+  struct HostGauss {
+    int d;
+    int dim() const { return d; }
+    void sample(rng::RngStream& g, std::span<double> out) const {
+      for (auto& v : out) v = g.next_gaussian();
+    }
+  };
+  auto g1 = rng::split_stream(rng::EngineKind::Mrg32k3a, 5, rng::StreamPartition{});
+  auto g2 = g1;
+  const auto a = quant::lloyd_build(quant::GaussianSampler{2}, 40, 2, 6, 3000, g1);
+  const auto b = quant::lloyd_build(HostGauss{2}, 40, 2, 6, 3000, g2);
+  REQUIRE(a.grid.size() == b.grid.size());
+  for (std::size_t i = 0; i < a.grid.data().size(); ++i) CHECK(a.grid.data()[i] == b.grid.data()[i]);
+  for (std::size_t i = 0; i < a.distortion.size(); ++i) CHECK(a.distortion[i] == b.distortion[i]);
+  const auto ea = quant::distortion(a.grid, quant::GaussianSampler{2}, 5000, g1);
+  const auto eb = quant::distortion(b.grid, HostGauss{2}, 5000, g2);
+  CHECK(ea.distortion == eb.distortion);
+  CHECK(ea.std_error == eb.std_error);
 }

@@ -13,7 +13,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "tests", "cpp", "_bin")
-PROGRAMS = ["ref_test_tree", "ref_test_pricer", "test_dropin"]
+PROGRAMS = ["ref_test_tree", "ref_test_pricer", "ref_test_quant", "test_dropin"]
 
 # Sections of the reference's tests that are undefined behaviour in the
 # reference itself and therefore cannot be judged: test_pricer.cpp:307-310
