@@ -72,6 +72,12 @@ _SIGS = {
     "qt_plan_fast_stats": [C.c_void_p, _u64p],
     "qt_fast_bounds_check": [_f64p],
     "qt_math_checksum": [C.c_int32, _u64p],
+    "qt_lloyd_build_stream": [C.c_int32, C.c_uint64, C.c_int32, C.c_uint64, _u64p,
+                              C.POINTER(C.c_int32), _f64p, _f64p, _f64p],
+    "qt_distortion_stream": [C.c_int32, C.c_uint64, _f64p, C.c_uint64, _u64p,
+                             C.POINTER(C.c_int32), _f64p, _f64p, _f64p],
+    "qt_lloyd_iterate": [C.c_int32, C.c_uint64, _f64p, C.c_uint64, _f64p, _f64p],
+    "qt_distortion_points": [C.c_int32, C.c_uint64, _f64p, C.c_uint64, _f64p, _f64p, _f64p],
     "qt_plan_cache_clear": [],
     "qt_payoff_table": [C.c_int32, C.c_int32, C.POINTER(QtModelParams), _f64p, C.c_int32, _u64p,
                         _f64p, _f64p],
