@@ -474,10 +474,11 @@ def run_ours(args, rank, world, local_rank):
     # algorithmic bytes of the path kernel: 16 B per transition (one u64 RMW)
     kern_units = count * n if est != 2 else count
     achieved = 16.0 * kern_units / (t_kern / 1e3) / 1e9
-    kernel_name = {"bm": "k_paths_fast + k_replay (certified 1-D path: MRG32k3a, FP32 Box-Muller "
-                         "with proven bounds, FP64 state, FP32 cell certificate, RED count; "
-                         "uncertified paths replayed exactly with the glibc-exact FP64 "
-                         "Box-Muller) + k_permute_add",
+    kernel_name = {"bm": "k_paths_x<CERT> + k_replay (certified 1-D path: MRG32k3a, approximate "
+                         "FP64 Box-Muller within an exhaustively verified bound of glibc's, "
+                         "state error bound, FP64 threshold-pair certificate, sorted-cell RED; "
+                         "uncertified paths (~0) replayed with the glibc-exact arithmetic) + "
+                         "k_permute_add",
                    "ou": "k_alg3_x (layer-parallel pair sampler)" if est == 2 else "k_paths_x",
                    "tf": "k_paths_cell (FP64 path + exact cell-list nearest-point search: "
                          "FP64 reference d2 over the bucket's candidate list)",

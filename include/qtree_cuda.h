@@ -314,14 +314,21 @@ QT_API qt_status qt_path_normals(int32_t engine, uint64_t seed, uint64_t normals
 QT_API qt_status qt_uniforms(int32_t engine, uint64_t seed, uint64_t offset, uint64_t count,
                              double* out);
 
-/* ---- fast 1-D path (Brownian / OU chains, MRG32k3a, Alg I/II) -------------
- * FP32 Box-Muller with a rigorous error bound; a transition is counted only
- * when the bounded FP64 state interval lies inside one cell, and a path with an
- * uncertified transition is recomputed with the exact FP64 arithmetic from that
- * layer on, so the counts equal the exact kernel's. Enabled by
- * default; QT_FAST_PATH=0 in the environment or qt_set_fast_path(0) selects
- * the exact kernel for every path. */
-QT_API qt_status qt_set_fast_path(int32_t enabled);
+/* ---- certified 1-D paths (Brownian / OU chains, MRG32k3a, Alg I/II) -------
+ * The kernel computes an approximate Box-Muller normal with a verified error
+ * bound, carries a bound on the path state's distance from the exact kernel's,
+ * and counts a transition only when every state within the bound lies in one
+ * cell; a path with an uncertified transition is recomputed with the exact FP64
+ * arithmetic from its start and counted from that layer on, so the counts equal
+ * the exact kernel's. mode: 2 = approximate FP64 normals on the
+ * x-tables (k_paths_x<CERT>, the default; uncertified paths ~1e-9), 1 = FP32
+ * normals on the fast tables (k_paths_fast; ~8 % replayed), 0 = the exact kernel
+ * for every path. Also QT_FAST_PATH=0/1/2 in the environment. */
+QT_API qt_status qt_set_fast_path(int32_t mode);
+/* out[7]: the measured maxima over all MRG32k3a uniforms of the certified kernel's
+ * approximate Box-Muller against the glibc-exact one (|r~-r|/r, |c~-c|, |s~-s|,
+ * max(|c~|,|s~|)) and the bounds the kernel assumes (kApxRadRel, kApxAng, kApxZ). */
+QT_API qt_status qt_apx_bounds_check(double* out);
 /* out[3] = {paths counted by the fast path, paths replayed exactly, paths
  * replayed inline after a replay-list overflow}, summed over destroyed plans. */
 QT_API qt_status qt_fast_stats(uint64_t* out);

@@ -72,6 +72,7 @@ _SIGS = {
     "qt_plan_fast_stats": [C.c_void_p, _u64p],
     "qt_fast_bounds_check": [_f64p],
     "qt_math_checksum": [C.c_int32, _u64p],
+    "qt_apx_bounds_check": [_f64p],
     "qt_lloyd_build_stream": [C.c_int32, C.c_uint64, C.c_int32, C.c_uint64, _u64p,
                               C.POINTER(C.c_int32), _f64p, _f64p, _f64p],
     "qt_distortion_stream": [C.c_int32, C.c_uint64, _f64p, C.c_uint64, _u64p,

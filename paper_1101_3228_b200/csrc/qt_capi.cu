@@ -34,6 +34,7 @@
 #include "../../include/qtree_cuda.h"
 #include "qt_internal.h"
 #include "qt_layout.h"
+#include "qt_math_fast.h"
 
 namespace {
 
@@ -65,15 +66,21 @@ bool cell_enabled() {
   return !(e && std::strcmp(e, "scan") == 0);
 }
 
-bool fast_enabled() {
+// 1-D MRG32k3a Alg I/II kernel: 0 = exact k_paths_x (glibc-exact Box-Muller for every
+// draw), 1 = k_paths_fast (FP32 Box-Muller, certified, exact replay), 2 = k_paths_x<CERT>
+// (approximate FP64 Box-Muller, certified, exact replay; the default).
+// QT_FAST_PATH=0/1/2 or qt_set_fast_path(mode).
+int mode1d() {
   int v = g_fast.load();
   if (v < 0) {
     const char* e = std::getenv("QT_FAST_PATH");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 1 : 2;
     g_fast.store(v);
   }
-  return v == 1;
+  return v;
 }
+bool fast_enabled() { return mode1d() == 1; }
+bool cert_enabled() { return mode1d() == 2; }
 
 struct Failure {
   qt_status code;
@@ -1065,7 +1072,7 @@ std::vector<uint8_t> plan_key(const qt_chain* chain, const qt_grids* grids, int 
     const uint8_t* b = static_cast<const uint8_t*>(p);
     k.insert(k.end(), b, b + n);
   };
-  const int32_t hdr[6] = {chain->kind, chain->layers, grids->dim, device, fast_enabled() ? 1 : 0,
+  const int32_t hdr[6] = {chain->kind, chain->layers, grids->dim, device, mode1d(),
                           cell_enabled() ? 1 : 0};
   put(hdr, sizeof hdr);
   const size_t n = static_cast<size_t>(chain->layers);
@@ -1155,12 +1162,16 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       if (const char* e = std::getenv("QT_FAST_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 2 ? 2 : 4;
       // fast tables: all resident when they fit, else prefetched S layers ahead
       const bool fres = p->total_ftab <= kResidentBudget;
-      // stages of two layers (k_paths_fast pairs the layers of one Box-Muller draw)
+      // stages of one or two layers (two: the pair of one Box-Muller draw); one
+      // measured faster at C2 (1.187e11 vs 1.119e11, profiles/r02_c2_variant_sweeps.txt)
+      uint32_t fl = 1;
+      if (const char* e = std::getenv("QT_FAST_L")) fl = std::atoi(e) == 1 ? 1u : 2u;
       uint32_t fbuf = p->max_ftab;
-      for (int k = 0; k < p->n; k += 2) {
-        const int k1 = std::min(k + 1, p->n - 1);
-        fbuf = std::max<uint32_t>(fbuf, p->ftab_off_h[k1] + p->ftab_bytes_h[k1] - p->ftab_off_h[k]);
-      }
+      if (fl == 2)
+        for (int k = 0; k < p->n; k += 2) {
+          const int k1 = std::min(k + 1, p->n - 1);
+          fbuf = std::max<uint32_t>(fbuf, p->ftab_off_h[k1] + p->ftab_bytes_h[k1] - p->ftab_off_h[k]);
+        }
       uint32_t st_n = 2;
       if (const char* e = std::getenv("QT_FAST_STAGES")) st_n = std::max(2, std::min(8, std::atoi(e)));
       const size_t fsmem = fres ? p->total_ftab : static_cast<size_t>(st_n) * fbuf;
@@ -1177,7 +1188,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       QT_CUDA(cudaMemsetAsync(p->d_sjoint, 0, p->njoint * sizeof(uint64_t), st));
       qt::FastArgs fa{fa_args, p->d_amb, p->d_stats, std::min(p->amb_cap, want),
                       p->d_ftables, p->d_ftab_off, p->d_ftab_bytes, fbuf, p->total_ftab,
-                      st_n, {}, std::getenv("QT_PROBE_NORED") ? 1u : 0u, p->d_sjoint};
+                      st_n, {}, std::getenv("QT_PROBE_NORED") ? 1u : 0u, p->d_sjoint, fl};
       mrg_back_jump(2 * ((static_cast<uint64_t>(p->n) + 1) / 2), fa.back);
       QT_CUDA(cudaMemsetAsync(p->d_stats, 0, sizeof(unsigned long long), st));
       QT_CUDA(qt::launch_paths_fast(p->kind, fres, P, fa, static_cast<uint32_t>(blocks), fsmem,
@@ -1216,9 +1227,30 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       xa.stages = Lp == 2 ? 2u : (3u * p->max_tab <= 150u * 1024u ? 3u : 2u);
       if (const char* e = std::getenv("QT_X_S")) xa.stages = std::max(2, std::min(8, std::atoi(e)));
       xa.probe_nored = std::getenv("QT_PROBE_NORED") ? 1u : 0u;
+      const bool cert = cert_enabled() && first + count <= (1ull << 48) && p->n < 65536;
+      if (cert) {  // the replay list: a certified path is rarely ambiguous (~1e-9)
+        const uint64_t want = std::max<uint64_t>(1u << 16, count / 1024 + 1);
+        if (!p->d_stats) {
+          QT_CUDA(cudaMalloc(&p->d_stats, 3 * sizeof(unsigned long long)));
+          QT_CUDA(cudaMemset(p->d_stats, 0, 3 * sizeof(unsigned long long)));
+        }
+        if (p->amb_cap < want) {
+          QT_CUDA(cudaFree(p->d_amb));
+          p->d_amb = nullptr;
+          p->amb_cap = 0;
+          QT_CUDA(cudaMalloc(&p->d_amb, want * sizeof(qt::AmbEntry)));
+          p->amb_cap = want;
+        }
+        QT_CUDA(cudaMemsetAsync(p->d_stats, 0, sizeof(unsigned long long), st));
+        xa.amb = p->d_amb;
+        xa.stats = p->d_stats;
+        xa.amb_cap = p->amb_cap;
+        xa.ojoint = reinterpret_cast<unsigned long long*>(d_joint);
+        mrg_back_jump(2 * ((static_cast<uint64_t>(p->n) + 1) / 2), xa.back);
+      }
       const size_t xsmem = resident ? p->total_tab : static_cast<size_t>(xa.stages) * buf;
       int xbps = 1;
-      QT_CUDA(qt::launch_paths_x(p->kind, resident, P, xa, 0, xsmem, st, &xbps));
+      QT_CUDA(qt::launch_paths_x(p->kind, resident, P, cert, xa, 0, xsmem, st, &xbps));
       uint64_t xblocks = static_cast<uint64_t>(p->sm_count) * xbps;
       const uint64_t per_block = static_cast<uint64_t>(qt::kXThreads) * P;
       const uint64_t xneed = (count + per_block - 1) / per_block;
@@ -1228,11 +1260,23 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       xa.rem = count % T;
       xa.joint = p->d_sjoint;
       xa.xtables = p->d_xtables;
-      QT_CUDA(qt::launch_paths_x(p->kind, resident, P, xa, static_cast<uint32_t>(xblocks), xsmem, st,
-                                 nullptr));
+      QT_CUDA(qt::launch_paths_x(p->kind, resident, P, cert, xa, static_cast<uint32_t>(xblocks),
+                                 xsmem, st, nullptr));
       QT_CUDA(qt::launch_permute_add(p->d_sjoint, reinterpret_cast<unsigned long long*>(d_joint),
                                      p->d_fin, p->d_orig, static_cast<uint32_t>(p->n),
                                      p->max_elems, st));
+      if (cert) {  // the exact replay of the uncertified paths, into the original-index counts
+        qt::FastArgs fr{};
+        fr.p = xa;
+        fr.p.joint = reinterpret_cast<unsigned long long*>(d_joint);
+        fr.amb = p->d_amb;
+        fr.stats = p->d_stats;
+        fr.cap = p->amb_cap;
+        QT_CUDA(qt::launch_replay(p->kind, fr, static_cast<uint32_t>(p->sm_count) * 4u, st));
+        p->fast_paths += count;
+        g_launches.fetch_add(3);
+        return 3;
+      }
       g_launches.fetch_add(2);
       return 2;
     }
@@ -2683,9 +2727,37 @@ QT_API qt_status qt_uniforms(int32_t engine, uint64_t seed, uint64_t offset, uin
   });
 }
 
-QT_API qt_status qt_set_fast_path(int32_t enabled) {
-  g_fast.store(enabled ? 1 : 0);
-  return QT_OK;
+// 1-D kernel selection (mode1d): 0 exact, 1 FP32 fast path, 2 certified FP64 (default)
+QT_API qt_status qt_set_fast_path(int32_t mode) {
+  return guarded([&] {
+    if (mode < 0 || mode > 2) raise(QT_ERR_INVALID_ARGUMENT, "set_fast_path: mode must be 0, 1 or 2");
+    g_fast.store(mode);
+  });
+}
+
+// Exhaustive bound check of the certified kernel's approximate Box-Muller
+// (qt_math_fast.h) against the glibc-exact one: out[0..3] as k_apx_bounds_check,
+// out[4..6] = the bounds the kernel uses (kApxRadRel, kApxAng, kApxZ).
+QT_API qt_status qt_apx_bounds_check(double* out) {
+  return guarded([&] {
+    if (!out) raise(QT_ERR_INVALID_ARGUMENT, "null argument");
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+      raise(QT_ERR_DEVICE, "cuda: no CUDA device available");
+    unsigned long long* d = nullptr;
+    QT_CUDA(cudaMalloc(&d, 4 * sizeof(unsigned long long)));
+    cudaError_t e = cudaMemset(d, 0, 4 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = qt::launch_apx_bounds_check(d, nullptr);
+    unsigned long long h[4] = {0, 0, 0, 0};
+    if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    QT_CUDA(e);
+    g_launches.fetch_add(1);
+    for (int i = 0; i < 4; ++i) std::memcpy(out + i, h + i, 8);
+    out[4] = qt::apx::kApxRadRel;
+    out[5] = qt::apx::kApxAng;
+    out[6] = qt::apx::kApxZ;
+  });
 }
 
 QT_API qt_status qt_fast_stats(uint64_t* out) {

@@ -51,6 +51,14 @@ struct SrcArgs {
   uint32_t per_unit;
 };
 
+// An uncertified path of the certified 1-D kernels (k_paths_fast, k_paths_x<CERT>),
+// replayed exactly by k_replay.
+struct AmbEntry {
+  unsigned long long key;  // (path << 16) | first uncertified layer
+  uint32_t st[6];          // MRG32k3a state at the path's first draw
+};
+static_assert(sizeof(AmbEntry) == 32, "AmbEntry is 32 bytes");
+
 struct PathArgs {
   SrcArgs src;
   const uint8_t* tables;      // layer tables, concatenated, 16-byte aligned
@@ -68,6 +76,13 @@ struct PathArgs {
   const uint8_t* xtables;     // k_paths_x: the d = 1 tables with Thr[] replaced by
                               // threshold pairs {t_c, t_c+1} (same offsets; counts are
                               // in sorted-cell space, see launch_permute_add)
+  // k_paths_x<CERT>: the uncertified paths' replay list and the original-index
+  // counts an overflowing list is replayed into inline
+  AmbEntry* amb;
+  unsigned long long* stats;  // [0] list entries of this launch, [1], [2] as FastArgs
+  uint64_t amb_cap;
+  unsigned long long* ojoint;
+  uint32_t back[18];          // (J^D)^-1: path end state -> path start state
 };
 
 constexpr int kPathConsumers = 256;  // consumer threads per k_paths CTA
@@ -78,13 +93,6 @@ constexpr int kPathConsumers = 256;  // consumer threads per k_paths CTA
 #define QT_X_THREADS 256
 #endif
 constexpr int kXThreads = QT_X_THREADS;  // k_paths_x CTA: warps in layer lockstep
-
-// Fast 1-D path (FP32 Box-Muller with certified cells + exact replay).
-struct AmbEntry {
-  unsigned long long key;  // (path << 16) | first uncertified layer
-  uint32_t st[6];          // MRG32k3a state at the path's first draw
-};
-static_assert(sizeof(AmbEntry) == 32, "AmbEntry is 32 bytes");
 
 struct FastArgs {
   PathArgs p;
@@ -102,6 +110,7 @@ struct FastArgs {
   uint32_t probe_nored;       // diagnostics only (QT_PROBE_NORED): skip the count REDs
   unsigned long long* sjoint; // certified counts, SORTED-cell space (launch_permute_add maps
                               // them to p.joint); replays count into p.joint directly
+  uint32_t flayers;           // layers per ring stage (1 or 2)
 };
 
 // d >= 2 FP32-scan path kernel (qt_scan.cu)
@@ -193,8 +202,10 @@ cudaError_t launch_pi(int engine, int skip, const SrcArgs& a, uint64_t samples, 
                       unsigned long long* inside, cudaStream_t st);
 cudaError_t launch_sum_u64(const unsigned long long* v, uint64_t n, unsigned long long* out,
                            cudaStream_t st);
-cudaError_t launch_paths_x(int kind, bool resident, int P, const PathArgs& a, uint32_t blocks,
-                           size_t smem, cudaStream_t st, int* bps);
+cudaError_t launch_paths_x(int kind, bool resident, int P, bool cert, const PathArgs& a,
+                           uint32_t blocks, size_t smem, cudaStream_t st, int* bps);
+cudaError_t launch_replay(int kind, const FastArgs& f, uint32_t blocks, cudaStream_t st);
+cudaError_t launch_apx_bounds_check(unsigned long long* out, cudaStream_t st);
 // joint[t][orig_t[a] N_{t+1} + orig_{t+1}[b]] += sjoint[t][a N_{t+1} + b] for every
 // layer t (sorted-cell counts of k_paths_x -> the reference's original indices);
 // fin = the finalize table (rows, cols, joff, voff_row, voff_col; 5 x n), orig

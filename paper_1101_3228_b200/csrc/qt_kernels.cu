@@ -26,6 +26,7 @@
 
 #include "qt_device.cuh"
 #include "qt_internal.h"
+#include "qt_math_fast.h"
 
 namespace qt {
 
@@ -243,7 +244,8 @@ __device__ __forceinline__ void fast_layer(FastPath (&ps)[P], const bool (&act)[
 
 // Replay of an ambiguous path from its stored start state (no jump-ahead).
 template <int K>
-__device__ __noinline__ void replay_entry(const PathArgs& a, const AmbEntry& ent) {
+__device__ __noinline__ void replay_entry(const PathArgs& a, unsigned long long* joint,
+                                          const AmbEntry& ent) {
   using C = Chain<K>;
   Source<kSrcMrg> src;
   src.s = Mrg{ent.st[0], ent.st[1], ent.st[2], ent.st[3], ent.st[4], ent.st[5]};
@@ -258,8 +260,9 @@ __device__ __noinline__ void replay_entry(const PathArgs& a, const AmbEntry& ent
     e[0] = src.normal();
     C::step(h.step, x, xn, e);
     x[0] = xn[0];
+    if (k + 1 < k0) continue;  // the prefix only needs the exact state, not its cells
     const uint32_t j = nearest_1d(h, tb, x[0], a.tables);
-    if (k >= k0) red_add_u64(a.joint + h.joff + static_cast<uint64_t>(i) * h.n_pts + j, 1ull);
+    if (k >= k0) red_add_u64(joint + h.joff + static_cast<uint64_t>(i) * h.n_pts + j, 1ull);
     i = j;
   }
 }
@@ -289,7 +292,9 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_fast(const __grid_consta
   __shared__ __align__(8) uint64_t full[kMaxStages];
   const uint32_t tid = threadIdx.x;
   const uint32_t S = f.fstages;
-  constexpr uint32_t L = 2;  // layers per stage: the pair sharing one Box-Muller draw
+  // layers per stage: 2 = the pair sharing one Box-Muller draw (one table wait and
+  // one barrier per pair), 1 = half the ring's shared memory (more CTAs per SM)
+  const uint32_t L = f.flayers == 1 ? 1u : 2u;
   const uint32_t spr = (a.n + L - 1) / L;
   const uint64_t rounds = a.q + (a.rem ? 1u : 0u);
   const uint64_t steps_total = rounds * spr;
@@ -355,7 +360,7 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_fast(const __grid_consta
         mbar_wait_u32(full0 + 8u * s, ph);
       }
       fast_layer<K, P>(ps, act, tb, k, f.sjoint, f.probe_nored == 0);
-      if (k + 1 <= a.n)
+      if (L == 2 && k + 1 <= a.n)
         fast_layer<K, P>(ps, act, tb + __ldg(f.ftab_bytes + k - 1), k + 1, f.sjoint,
                          f.probe_nored == 0);
       if constexpr (!RESIDENT) {
@@ -386,7 +391,7 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_fast(const __grid_consta
         if (idx < f.cap) {
           f.amb[idx] = ent;
         } else {  // list full: replay here (correct, slow; never expected)
-          replay_entry<K>(a, ent);
+          replay_entry<K>(a, a.joint, ent);
           atomicAdd(f.stats + 2, 1ull);
         }
       }
@@ -404,9 +409,15 @@ __global__ void __launch_bounds__(kFastThreads) k_paths_fast(const __grid_consta
 // ---------------------------------------------------------------------------
 struct ExactPath {
   Mrg st;
-  double x;     // state (chains.hpp: origin at the path start)
+  double x;     // state (chains.hpp: origin at the path start); CERT: x~
   double zs;    // Box-Muller mate
   uint32_t i;   // cell at the previous layer
+  // CERT only: |x~ - x| <= e against the exact kernel's state x, the mate's
+  // bound (both FP32, rounded up), and the first layer whose cell was not
+  // certified (0: none yet)
+  float e;
+  float bzs;
+  uint32_t amb_k;
 };
 
 // Sorted position (not the original index) of the exact scan's answer: the
@@ -449,7 +460,7 @@ __device__ __forceinline__ uint32_t nearest_1d_pos(const LayerTable& h, const ui
 // two-step bracket), and the cell is kept as its SORTED position c; the
 // counts land in sorted-cell space (sjoint) and launch_permute_add maps them
 // to the reference's original indices once per count call.
-template <int K, int P>
+template <int K, int P, bool CERT>
 __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act)[P],
                                             const uint8_t* tb, uint32_t k,
                                             unsigned long long* joint, const uint8_t* gtables,
@@ -462,6 +473,7 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
   const uint16_t* start = reinterpret_cast<const uint16_t*>(tb + h.off_start);
   unsigned long long* jl = joint + h.joff;
   double z[P];
+  float bz[P];
   if (k & 1u) {  // a fresh pair (stream.hpp:97-108): z1 now, z2 cached
     double u1[P], u2[P], zs[P];
 #pragma unroll
@@ -471,12 +483,28 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
       u1[p] = mrg_to_unit(a1);
       u2[p] = mrg_to_unit(a2);
     }
-    box_muller_batch<P>(u1, u2, z, zs);
+    if constexpr (CERT) {  // approximate FP64 pair with its verified bound (qt_math_fast.h)
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const double r = __dsqrt_rn(__dmul_rn(-2.0, apx::log_unit(u1[p])));
+        double sn, cs;
+        apx::sincos(__dmul_rn(kTwoPi, u2[p]), &sn, &cs);
+        z[p] = __dmul_rn(r, cs);
+        zs[p] = __dmul_rn(r, sn);
+        bz[p] = __double2float_ru(__dmul_ru(r, apx::kApxZ));
+        ps[p].bzs = bz[p];
+      }
+    } else {
+      box_muller_batch<P>(u1, u2, z, zs);
+    }
 #pragma unroll
     for (int p = 0; p < P; ++p) ps[p].zs = zs[p];
   } else {
 #pragma unroll
-    for (int p = 0; p < P; ++p) z[p] = ps[p].zs;
+    for (int p = 0; p < P; ++p) {
+      z[p] = ps[p].zs;
+      if constexpr (CERT) bz[p] = ps[p].bzs;
+    }
   }
   uint32_t c[P];
   bool safe[P];
@@ -484,29 +512,64 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
   for (int p = 0; p < P; ++p) {
     double xn[1], e[1] = {z[p]}, xo[1] = {ps[p].x};
     C::step(h.step, xo, xn, e);
+    if constexpr (CERT) {
+      // e' >= |x~' - x'| for x' = RN(RN(a x) + RN(s z)) (Brownian: a = 1, no
+      // product): |a| e + |s| bz, plus 2^-50 of every operand for the roundings
+      // that may differ; FP32 with every operation rounded up (fa, fs >= |a|, |s|)
+      const float fa = h.fa, fs = h.fs;
+      const float lin = __fmaf_ru(fa, ps[p].e, __fmul_ru(fs, bz[p]));
+      const float mag = __fmaf_ru(fa, __double2float_ru(fabs(xo[0])),
+                                  __fmaf_ru(fs, __double2float_ru(fabs(z[p])),
+                                            __double2float_ru(fabs(xn[0]))));
+      ps[p].e = __fmaf_ru(mag, 0x1p-50f, __fmaf_ru(lin, 0x1p-50f, lin));
+      const double ed = static_cast<double>(ps[p].e);
+      const double xl = __dsub_rd(xn[0], ed);
+      safe[p] = __dadd_ru(fabs(xn[0]), ed) < x_safe;
+      c[p] = start[bucket_of(safe[p] ? xl : 0.0, lo, inv_w, nb_d, nb)];  // all t_{<c} < xl
+    } else {
+      safe[p] = fabs(xn[0]) < x_safe;
+      c[p] = start[bucket_of(safe[p] ? xn[0] : 0.0, lo, inv_w, nb_d, nb)];  // all t_{<c} < x
+    }
     ps[p].x = xn[0];
-    safe[p] = fabs(xn[0]) < x_safe;
-    c[p] = start[bucket_of(safe[p] ? xn[0] : 0.0, lo, inv_w, nb_d, nb)];  // all t_{<c} < x
   }
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     const double x = ps[p].x;
     uint32_t j;
-    if (safe[p]) {
+    if constexpr (CERT) {
+      // the cell of every state in [x~ - e, x~ + e]: c if xh < t_c, c + 1 if
+      // t_c <= xl and xh < t_c+1; anything else (or |x| near x_safe) is not
+      // certified and the path is replayed exactly from its start
+      const double ed = static_cast<double>(ps[p].e);
+      const double xl = __dsub_rd(x, ed), xh = __dadd_ru(x, ed);
       const double2 r = PT[c[p]];
-      if (x < r.x) {
-        j = c[p];
-      } else if (x < r.y) {
-        j = c[p] + 1;
-      } else {
-        uint32_t cc = c[p] + 2;
-        while (!(x < PT[cc].x)) ++cc;  // t_{N-1} = +inf stops the walk
-        j = cc;
+      const bool in0 = xh < r.x;
+      const bool in1 = !(xl < r.x) && xh < r.y;
+      j = in0 ? c[p] : c[p] + 1;
+      if (act[p] && ps[p].amb_k == 0) {
+        if (safe[p] && (in0 || in1)) {
+          if (count) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + j, 1ull);
+        } else {
+          ps[p].amb_k = k;
+        }
       }
-    } else {  // exact scan over the cold block (NaN / inf / |x| >= x_safe)
-      j = nearest_1d_scan_pos(reinterpret_cast<const Rec1*>(gtables + h.cold_off), npts, x);
+    } else {
+      if (safe[p]) {
+        const double2 r = PT[c[p]];
+        if (x < r.x) {
+          j = c[p];
+        } else if (x < r.y) {
+          j = c[p] + 1;
+        } else {
+          uint32_t cc = c[p] + 2;
+          while (!(x < PT[cc].x)) ++cc;  // t_{N-1} = +inf stops the walk
+          j = cc;
+        }
+      } else {  // exact scan over the cold block (NaN / inf / |x| >= x_safe)
+        j = nearest_1d_scan_pos(reinterpret_cast<const Rec1*>(gtables + h.cold_off), npts, x);
+      }
+      if (act[p] && count) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + j, 1ull);
     }
-    if (act[p] && count) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + j, 1ull);
     ps[p].i = j;
   }
 }
@@ -514,7 +577,7 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
 // L = layers per pipeline stage: with L = 2 one stage holds the (contiguous)
 // tables of layers 2q+1 and 2q+2, which share one Box-Muller pair, so the table
 // wait and the barrier are paid once per two layers.
-template <int K, bool RESIDENT, int P, int L>
+template <int K, bool RESIDENT, int P, int L, bool CERT>
 __global__ void __launch_bounds__(kXThreads, QT_X_MINB) k_paths_x(const __grid_constant__ PathArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
@@ -574,6 +637,8 @@ __global__ void __launch_bounds__(kXThreads, QT_X_MINB) k_paths_x(const __grid_c
       act[p] = r < cnt[p];
       ps[p].x = 0.0;  // chains.hpp:43-46,81: the origin
       ps[p].i = 0;    // layer 0 is the singleton {x0}
+      ps[p].e = 0.0f;
+      ps[p].amb_k = 0;
     }
     for (uint32_t k = 1; k <= a.n; k += L, ++g) {
       if constexpr (RESIDENT) {
@@ -581,10 +646,10 @@ __global__ void __launch_bounds__(kXThreads, QT_X_MINB) k_paths_x(const __grid_c
       } else {
         mbar_wait_u32(full0 + 8u * s, ph);
       }
-      exact_layer<K, P>(ps, act, tb, k, a.joint, a.tables, a.probe_nored == 0);
+      exact_layer<K, P, CERT>(ps, act, tb, k, a.joint, a.tables, a.probe_nored == 0);
       if (L == 2 && k + 1 <= a.n)  // the next table follows this one (header.bytes)
-        exact_layer<K, P>(ps, act, tb + reinterpret_cast<const LayerTable*>(tb)->bytes, k + 1,
-                          a.joint, a.tables, a.probe_nored == 0);
+        exact_layer<K, P, CERT>(ps, act, tb + reinterpret_cast<const LayerTable*>(tb)->bytes,
+                                k + 1, a.joint, a.tables, a.probe_nored == 0);
       if constexpr (!RESIDENT) {
         named_barrier_sync(1, kXThreads);  // every thread is done with stage s
         if (tid == 0 && g + S < steps_total) issue(g + S);
@@ -596,13 +661,39 @@ __global__ void __launch_bounds__(kXThreads, QT_X_MINB) k_paths_x(const __grid_c
         }
       }
     }
+    if constexpr (CERT) {  // uncertified paths -> the replay list (path start state)
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        if (act[p] && ps[p].amb_k != 0) {
+          const uint64_t v = gid * P + p;
+          const uint64_t beg = a.first + v * a.q + (v < a.rem ? v : a.rem);
+          AmbEntry ent;
+          ent.key = ((beg + r) << 16) | ps[p].amb_k;
+          Mrg st0 = ps[p].st;
+          mrg_apply(a.back, st0);
+          ent.st[0] = st0.a0;
+          ent.st[1] = st0.a1;
+          ent.st[2] = st0.a2;
+          ent.st[3] = st0.b0;
+          ent.st[4] = st0.b1;
+          ent.st[5] = st0.b2;
+          const unsigned long long idx = atomicAdd(a.stats, 1ull);
+          if (idx < a.amb_cap) {
+            a.amb[idx] = ent;
+          } else {  // list full: replay here into the original-index counts
+            replay_entry<K>(a, a.ojoint, ent);
+            atomicAdd(a.stats + 2, 1ull);
+          }
+        }
+      }
+    }
   }
 }
 
-template <int K, bool RES, int P>
+template <int K, bool RES, int P, bool CERT>
 static cudaError_t launch_x_t(const PathArgs& a, uint32_t blocks, size_t smem, cudaStream_t st,
                               int* bps) {
-  auto fn = a.layers_per_stage == 2 ? k_paths_x<K, RES, P, 2> : k_paths_x<K, RES, P, 1>;
+  auto fn = a.layers_per_stage == 2 ? k_paths_x<K, RES, P, 2, CERT> : k_paths_x<K, RES, P, 1, CERT>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -617,24 +708,37 @@ static cudaError_t launch_x_t(const PathArgs& a, uint32_t blocks, size_t smem, c
 }
 
 template <int K>
-static cudaError_t launch_x_k(bool res, int P, const PathArgs& a, uint32_t blocks, size_t smem,
-                              cudaStream_t st, int* bps) {
+static cudaError_t launch_x_k(bool res, int P, bool cert, const PathArgs& a, uint32_t blocks,
+                              size_t smem, cudaStream_t st, int* bps) {
+  if (cert) {
+    if (P == 1)
+      return res ? launch_x_t<K, true, 1, true>(a, blocks, smem, st, bps)
+                 : launch_x_t<K, false, 1, true>(a, blocks, smem, st, bps);
+    if (P == 4)
+      return res ? launch_x_t<K, true, 4, true>(a, blocks, smem, st, bps)
+                 : launch_x_t<K, false, 4, true>(a, blocks, smem, st, bps);
+    return res ? launch_x_t<K, true, 2, true>(a, blocks, smem, st, bps)
+               : launch_x_t<K, false, 2, true>(a, blocks, smem, st, bps);
+  }
   if (P == 1)
-    return res ? launch_x_t<K, true, 1>(a, blocks, smem, st, bps)
-               : launch_x_t<K, false, 1>(a, blocks, smem, st, bps);
+    return res ? launch_x_t<K, true, 1, false>(a, blocks, smem, st, bps)
+               : launch_x_t<K, false, 1, false>(a, blocks, smem, st, bps);
   if (P == 4)
-    return res ? launch_x_t<K, true, 4>(a, blocks, smem, st, bps)
-               : launch_x_t<K, false, 4>(a, blocks, smem, st, bps);
-  return res ? launch_x_t<K, true, 2>(a, blocks, smem, st, bps)
-             : launch_x_t<K, false, 2>(a, blocks, smem, st, bps);
+    return res ? launch_x_t<K, true, 4, false>(a, blocks, smem, st, bps)
+               : launch_x_t<K, false, 4, false>(a, blocks, smem, st, bps);
+  return res ? launch_x_t<K, true, 2, false>(a, blocks, smem, st, bps)
+             : launch_x_t<K, false, 2, false>(a, blocks, smem, st, bps);
 }
 
-// k_paths_x (kind 0 = Brownian, 2 = OU; MRG32k3a). bps != nullptr: occupancy query only.
-cudaError_t launch_paths_x(int kind, bool resident, int P, const PathArgs& a, uint32_t blocks,
-                           size_t smem, cudaStream_t st, int* bps) {
-  return kind == 0 ? launch_x_k<0>(resident, P, a, blocks, smem, st, bps)
-                   : launch_x_k<2>(resident, P, a, blocks, smem, st, bps);
+// k_paths_x (kind 0 = Brownian, 2 = OU; MRG32k3a); cert: the certified variant
+// (approximate FP64 Box-Muller, uncertified paths to a.amb). bps != nullptr:
+// occupancy query only.
+cudaError_t launch_paths_x(int kind, bool resident, int P, bool cert, const PathArgs& a,
+                           uint32_t blocks, size_t smem, cudaStream_t st, int* bps) {
+  return kind == 0 ? launch_x_k<0>(resident, P, cert, a, blocks, smem, st, bps)
+                   : launch_x_k<2>(resident, P, cert, a, blocks, smem, st, bps);
 }
+
 
 // The replay list of one k_paths_fast launch, grid-stride.
 template <int K>
@@ -644,7 +748,14 @@ __global__ void __launch_bounds__(256) k_replay(const __grid_constant__ FastArgs
   const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g0 == 0) atomicAdd(f.stats + 1, static_cast<unsigned long long>(n));
   for (uint64_t g = g0; g < n; g += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    replay_entry<K>(f.p, f.amb[g]);
+    replay_entry<K>(f.p, f.p.joint, f.amb[g]);
+}
+
+// The replay list of a certified launch (k_paths_x<CERT> or k_paths_fast), grid-stride.
+cudaError_t launch_replay(int kind, const FastArgs& f, uint32_t blocks, cudaStream_t st) {
+  if (kind == 0) k_replay<0><<<blocks, 256, 0, st>>>(f);
+  else k_replay<2><<<blocks, 256, 0, st>>>(f);
+  return cudaGetLastError();
 }
 
 // Exhaustive check of the FP32 Box-Muller bounds over all 2^32 - 209 MRG32k3a
@@ -1207,6 +1318,38 @@ int paths_fast_blocks_per_sm(int kind, bool resident, int P, size_t smem) {
 
 cudaError_t launch_math_checksum(int domain, unsigned long long* out, cudaStream_t st) {
   k_math_checksum<<<148 * 16, 256, 0, st>>>(domain, out);
+  return cudaGetLastError();
+}
+
+// Exhaustive check of qt_math_fast.h against the glibc-exact pair over all
+// 2^32 - 209 MRG32k3a outputs x (as u1 and as u2): out[0] = max |r~ - r| / r,
+// out[1] = max |c~ - c|, out[2] = max |s~ - s|, out[3] = max(|c~|, |s~|), as
+// the bit patterns of non-negative doubles (which order like their bits).
+__global__ void __launch_bounds__(256) k_apx_bounds_check(unsigned long long* out) {
+  double m0 = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
+  for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < kM1;
+       g += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const double u = mrg_to_unit(static_cast<uint32_t>(g));
+    const double r = __dsqrt_rn(__dmul_rn(-2.0, qt_log_unit(u)));
+    const double ra = __dsqrt_rn(__dmul_rn(-2.0, apx::log_unit(u)));
+    if (r > 0.0) m0 = fmax(m0, fabs(ra - r) / r);
+    else if (ra != 0.0) m0 = 1.0;  // u = 1: both must give 0
+    const double a = __dmul_rn(kTwoPi, u);
+    double s, c, sa, ca;
+    qt_sincos_2pi(a, &s, &c);
+    apx::sincos(a, &sa, &ca);
+    m1 = fmax(m1, fabs(ca - c));
+    m2 = fmax(m2, fabs(sa - s));
+    m3 = fmax(m3, fmax(fabs(ca), fabs(sa)));
+  }
+  atomicMax(out + 0, static_cast<unsigned long long>(__double_as_longlong(m0)));
+  atomicMax(out + 1, static_cast<unsigned long long>(__double_as_longlong(m1)));
+  atomicMax(out + 2, static_cast<unsigned long long>(__double_as_longlong(m2)));
+  atomicMax(out + 3, static_cast<unsigned long long>(__double_as_longlong(m3)));
+}
+
+cudaError_t launch_apx_bounds_check(unsigned long long* out, cudaStream_t st) {
+  k_apx_bounds_check<<<148 * 16, 256, 0, st>>>(out);
   return cudaGetLastError();
 }
 

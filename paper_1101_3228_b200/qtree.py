@@ -557,10 +557,23 @@ def plan_cache_clear() -> None:
     _check(L.lib().qt_plan_cache_clear(), "plan_cache_clear")
 
 
-def set_fast_path(enabled: bool) -> None:
-    """Select the fast 1-D path (FP32 Box-Muller + certified cells + exact
-    replay; identical counts) or the exact FP64 kernel for every path."""
-    L.lib().qt_set_fast_path(1 if enabled else 0)
+CERTIFIED_1D, FAST_FP32_1D, EXACT_1D = 2, 1, 0
+
+
+def set_fast_path(mode) -> None:
+    """1-D MRG32k3a kernel (identical counts in every mode): 2 = certified with
+    approximate FP64 normals (the default), True / 1 = certified with FP32
+    normals (k_paths_fast), False / 0 = the exact kernel for every path."""
+    m = int(mode) if not isinstance(mode, bool) else (1 if mode else 0)
+    _check(L.lib().qt_set_fast_path(m), "set_fast_path")
+
+
+def apx_bounds_check() -> np.ndarray:
+    """Measured maxima of the certified kernel's approximate Box-Muller vs the
+    glibc-exact one over all MRG32k3a uniforms, and the bounds it assumes."""
+    out = np.zeros(7, np.float64)
+    _check(L.lib().qt_apx_bounds_check(_f(out)), "apx_bounds_check")
+    return out
 
 
 def fast_stats() -> dict:

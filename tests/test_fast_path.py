@@ -30,11 +30,11 @@ def Q():
 
 @pytest.fixture(autouse=True)
 def fast_on():
-    """The fast path is the default (QT_FAST_PATH=0 / set_fast_path(False)
-    selects the exact kernel); each test starts and ends with it enabled."""
+    """These tests select the FP32 certified kernel (set_fast_path(True)); each
+    ends by restoring the default (the certified FP64 kernel, mode 2)."""
     Q().set_fast_path(True)
     yield
-    Q().set_fast_path(True)
+    Q().set_fast_path(2)
 
 
 def _counts(plan, M, first=0, total=None, fast=True):
@@ -169,3 +169,55 @@ def test_xtables_equal_thr_kernels_adversarial_grids(gpu, case, monkeypatch):
         ref = q.estimate(alg, ch, grids, M)
         assert np.array_equal(x.flat_joint, ref.flat_joint), (case, alg)
         assert np.array_equal(x.flat_visits, ref.flat_visits), (case, alg)
+
+
+# --- the certified FP64 kernel (the default, k_paths_x<CERT>) ----------------------
+
+def test_apx_box_muller_bounds_exhaustive(gpu):
+    """qt_math_fast.h vs the glibc-exact pair over every MRG32k3a output: the
+    measured maxima must sit inside the bounds the certified kernel assumes."""
+    out = Q().apx_bounds_check()
+    rad, ang_c, ang_s, mag, k_rad, k_ang, k_z = (float(v) for v in out)
+    assert rad <= k_rad, (rad, k_rad)
+    assert ang_c <= k_ang and ang_s <= k_ang, (ang_c, ang_s, k_ang)
+    assert mag <= 1.0, mag
+    assert k_z >= (k_rad + k_ang + 2.0**-52) * (1 + 2.0**-40)
+
+
+@pytest.mark.parametrize("kind", ["bm", "ou"])
+def test_certified_fp64_equals_exact(gpu, kind):
+    """Mode 2 (the default) equals the exact kernel on C2- and C3-shaped chains,
+    at path windows deep in a 1e9-path stream."""
+    from paper_1101_3228_b200.device import Plan
+    q = Q()
+    if kind == "bm":
+        ch = q.BrownianChain1d(50)
+        grids = q.build_brownian_grids(ch, 500)
+    else:
+        p = q.TwoFactorParams(sigma1=0.5, alpha1=1.0, sigma2=0.0, steps=60)
+        ch = q.OuChain1d(p)
+        grids = q.build_ou_grids(ch, 200)
+    plan = Plan(ch, grids, 0)
+    for first in (0, 555555555):
+        cert = _counts(plan, 10**6, first, 10**9, 2)
+        exact = _counts(plan, 10**6, first, 10**9, False)
+        assert np.array_equal(cert, exact), (kind, first)
+
+
+def test_certified_fp64_replays_adversarial(gpu):
+    """A grid with cells narrower than the state bound (1e-14 wide pairs) makes
+    most paths uncertified: the replay must still give the exact counts,
+    including the inline replay when the list overflows."""
+    from paper_1101_3228_b200.device import Plan
+    q = Q()
+    ch = q.BrownianChain1d(8)
+    rng = np.random.default_rng(4)
+    grids = []
+    for k in range(1, 9):
+        base = np.sort(rng.standard_normal(40)) * np.sqrt(k / 8)
+        pts = np.concatenate([base, base + 3e-14 * (1 + np.abs(base))])
+        grids.append(q.QuantGrid(1, pts))
+    plan = Plan(ch, grids, 0)
+    cert = _counts(plan, 200000, 0, None, 2)
+    exact = _counts(plan, 200000, 0, None, False)
+    assert np.array_equal(cert, exact)

@@ -1,8 +1,9 @@
 # Round-end evidence on one B200, in parts (gpurun returns <= 64 MiB per call):
 #   PART=bench  bench lines (all configs), the reference arm, the launch list of
 #               the default bench command
-#   PART=traffic  DRAM bytes of the full-size C2 count launch (M = 1e9)
-#   PART=kx     ncu --set full of k_paths_x (C2 grids, 1e9 transitions)
+#   PART=traffic  DRAM bytes of the full-size C2 count launch (M = 1e9, k_paths_fast)
+#   PART=kx     ncu --set full of k_paths_x (C2 grids, 1e9 transitions, QT_FAST_PATH=0)
+#   PART=fast   ncu --set full of k_paths_fast (C2 grids, 1e9 transitions)
 #   PART=c4     ncu --set full of the d >= 2 path kernel (C4, 3.65e8 transitions)
 #   PART=c5     the same for C5 (8e6 transitions)
 #   PART=c3     ncu --set full of k_alg3_x (C3, 3.65e8 samples)
@@ -12,17 +13,18 @@ O=gpurun_out
 mkdir -p $O
 case ${PART:-bench} in
 bench)
-  python bench.py > $O/${TAG}_bench_c2.json 2> $O/${TAG}_bench_c2.err
-  python bench.py --impl reference > $O/${TAG}_bench_ref.json 2>&1
-  for c in c1 c3 c4 c5; do python bench.py --config $c > $O/${TAG}_bench_$c.json 2> $O/${TAG}_bench_$c.err; done
+  bash tools/bench_all.sh
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches_c2_default.csv \
       python bench.py --no-cpu-baseline > $O/${TAG}_launches_bench.log 2>&1 ;;
 traffic)
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-      -k regex:k_paths_x -c 1 --csv --log-file $O/${TAG}_traffic_c2.csv \
+      -k regex:k_paths_fast -c 1 --csv --log-file $O/${TAG}_traffic_c2.csv \
       python bench.py --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 1 > $O/${TAG}_traffic.log 2>&1 ;;
+fast)
+  ncu --set full --clock-control none --import-source on -k regex:k_paths_fast -c 1 -o $O/${TAG}_fast \
+      python bench.py --paths 2e7 --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 1 > $O/${TAG}_ncu_fast.log 2>&1 ;;
 kx)
-  ncu --set full --clock-control none --import-source on -k regex:k_paths_x -c 1 -o $O/${TAG}_kx \
+  QT_FAST_PATH=0 ncu --set full --clock-control none --import-source on -k regex:k_paths_x -c 1 -o $O/${TAG}_kx \
       python bench.py --paths 2e7 --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 1 > $O/${TAG}_ncu_kx.log 2>&1 ;;
 c4)
   ncu --set full --clock-control none --import-source on -k regex:"k_paths_(scan|cell)" -c 1 -o $O/${TAG}_c4 \
