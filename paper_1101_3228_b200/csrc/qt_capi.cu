@@ -732,8 +732,8 @@ TableBlob build_table(int kind, int dim, uint64_t npts, const double* pts, const
     }
     h.lo = lo;
     h.inv_w = inv_w;
-    h.bk_a = static_cast<float>(inv_w);
-    h.bk_b = static_cast<float>(-lo * inv_w);
+    h.cert_c = 0.0f;     // set on the x-tables (make_plan), which know layer k-1
+    h.cert_xmax = 0.0f;
     h.x_safe = x_safe;
     h.nb = nb;
     h.nb_d = static_cast<double>(nb);
@@ -960,6 +960,23 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
         PT[2 * c + 1] = T[c + 1].t;
       }
       PT[2 * N] = PT[2 * N + 1] = std::numeric_limits<double>::infinity();
+    }
+    // the certified kernel's per-layer state range X_k and rounding term (LayerTable)
+    double xprev = 0.0;  // layer 0: the origin
+    for (int k = 1; k <= n; ++k) {
+      uint8_t* tb = xtables.data() + p->tab_off[k - 1];
+      qt::LayerTable& h = *reinterpret_cast<qt::LayerTable*>(tb);
+      const double* PT = reinterpret_cast<const double*>(tb + h.off_rec);
+      const uint64_t N = p->sizes[k];
+      double X = 1e6;  // a single cell takes every state
+      if (N >= 2) X = 8.0 * std::max(std::fabs(PT[0]), std::fabs(PT[2 * (N - 2)]));
+      X = std::min(X, h.x_safe);
+      float xmax = static_cast<float>(X);
+      if (static_cast<double>(xmax) > X) xmax = std::nextafter(xmax, 0.0f);
+      h.cert_xmax = xmax > 0.0f ? xmax : 0.0f;
+      const double mag = static_cast<double>(h.fa) * xprev + static_cast<double>(h.fs) * 6.7 + X;
+      h.cert_c = f32_up(mag * 0x1p-50 * (1.0 + 0x1p-30));
+      xprev = static_cast<double>(h.cert_xmax);
     }
   }
   // FP32 scan tables (d >= 2)

@@ -516,15 +516,13 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
       // e' >= |x~' - x'| for x' = RN(RN(a x) + RN(s z)) (Brownian: a = 1, no
       // product): |a| e + |s| bz, plus 2^-50 of every operand for the roundings
       // that may differ; FP32 with every operation rounded up (fa, fs >= |a|, |s|)
-      const float fa = h.fa, fs = h.fs;
-      const float lin = __fmaf_ru(fa, ps[p].e, __fmul_ru(fs, bz[p]));
-      const float mag = __fmaf_ru(fa, __double2float_ru(fabs(xo[0])),
-                                  __fmaf_ru(fs, __double2float_ru(fabs(z[p])),
-                                            __double2float_ru(fabs(xn[0]))));
-      ps[p].e = __fmaf_ru(mag, 0x1p-50f, __fmaf_ru(lin, 0x1p-50f, lin));
+      // |x_{k-1}| < X_{k-1} (certified, or the origin) and |x_k| < X_k (checked
+      // below) bound those operands: the per-layer h.cert_c (make_plan)
+      const float lin = __fmaf_ru(h.fa, ps[p].e, __fmul_ru(h.fs, bz[p]));
+      ps[p].e = __fadd_ru(__fmaf_ru(lin, 0x1p-50f, lin), h.cert_c);
       const double ed = static_cast<double>(ps[p].e);
       const double xl = __dsub_rd(xn[0], ed);
-      safe[p] = __dadd_ru(fabs(xn[0]), ed) < x_safe;
+      safe[p] = __dadd_ru(fabs(xn[0]), ed) < static_cast<double>(h.cert_xmax);
       c[p] = start[bucket_of(safe[p] ? xl : 0.0, lo, inv_w, nb_d, nb)];  // all t_{<c} < xl
     } else {
       safe[p] = fabs(xn[0]) < x_safe;

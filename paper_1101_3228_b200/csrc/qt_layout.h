@@ -45,8 +45,10 @@ struct alignas(16) LayerTable {
   uint32_t dim;
   float fa;             // d == 1 fast path: |a| of x' = a x + s eps, rounded up (FP32)
   float fs;             // d == 1 fast path: |s|, rounded up (FP32)
-  float bk_a, bk_b;     // d == 1 fast path: approximate bucket fma(x, bk_a, bk_b)
-                        // (FP32; any start cell is fine there, certification decides)
+  float cert_c;         // d == 1 certified path (x-tables): RU(2^-50 (|a| X_{k-1} + |s| 6.7 + X_k)),
+                        // the rounding term of the state bound for |x_{k-1}| < X_{k-1}, |x_k| < X_k
+  float cert_xmax;      // d == 1 certified path: X_k = min(x_safe, 8 max |t|) rounded down;
+                        // a state beyond it is not certified (replayed)
 };
 static_assert(sizeof(LayerTable) == 192, "LayerTable header is 192 bytes");
 
