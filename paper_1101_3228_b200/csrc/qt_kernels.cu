@@ -486,7 +486,7 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
     if constexpr (CERT) {  // approximate FP64 pair with its verified bound (qt_math_fast.h)
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        const double r = __dsqrt_rn(__dmul_rn(-2.0, apx::log_unit(u1[p])));
+        const double r = apx::radius(u1[p]);
         double sn, cs;
         apx::sincos(__dmul_rn(kTwoPi, u2[p]), &sn, &cs);
         z[p] = __dmul_rn(r, cs);
@@ -1329,7 +1329,7 @@ __global__ void __launch_bounds__(256) k_apx_bounds_check(unsigned long long* ou
        g += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const double u = mrg_to_unit(static_cast<uint32_t>(g));
     const double r = __dsqrt_rn(__dmul_rn(-2.0, qt_log_unit(u)));
-    const double ra = __dsqrt_rn(__dmul_rn(-2.0, apx::log_unit(u)));
+    const double ra = apx::radius(u);
     if (r > 0.0) m0 = fmax(m0, fabs(ra - r) / r);
     else if (ra != 0.0) m0 = 1.0;  // u = 1: both must give 0
     const double a = __dmul_rn(kTwoPi, u);
