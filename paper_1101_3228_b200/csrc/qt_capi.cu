@@ -1389,12 +1389,39 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       QT_CUDA(cudaMemsetAsync(p->d_sjoint, 0, p->njoint * sizeof(uint64_t), st));
       a.joint = p->d_sjoint;
       a.xtables = p->d_xtables;
-      QT_CUDA(qt::launch_alg3_x(p->kind, P, a, static_cast<uint32_t>(slices), smem, st));
+      const bool cert = cert_enabled() && first + count <= (1ull << 48) && p->n < 65536;
+      if (cert) {  // uncertified samples -> k_replay3 (none expected at C3)
+        const uint64_t want = std::max<uint64_t>(1u << 16, count / 1024 + 1);
+        if (!p->d_stats) {
+          QT_CUDA(cudaMalloc(&p->d_stats, 3 * sizeof(unsigned long long)));
+          QT_CUDA(cudaMemset(p->d_stats, 0, 3 * sizeof(unsigned long long)));
+        }
+        if (p->amb_cap < want) {
+          QT_CUDA(cudaFree(p->d_amb));
+          p->d_amb = nullptr;
+          p->amb_cap = 0;
+          QT_CUDA(cudaMalloc(&p->d_amb, want * sizeof(qt::AmbEntry)));
+          p->amb_cap = want;
+        }
+        QT_CUDA(cudaMemsetAsync(p->d_stats, 0, sizeof(unsigned long long), st));
+        a.amb = p->d_amb;
+        a.stats = p->d_stats;
+        a.amb_cap = p->amb_cap;
+        a.ojoint = reinterpret_cast<unsigned long long*>(d_joint);
+        mrg_back_jump(2, a.back2);
+        if (P == 4) P = 2;
+      }
+      QT_CUDA(qt::launch_alg3_x(p->kind, P, cert, a, static_cast<uint32_t>(slices), smem, st));
       QT_CUDA(qt::launch_permute_add(p->d_sjoint, reinterpret_cast<unsigned long long*>(d_joint),
                                      p->d_fin, p->d_orig, static_cast<uint32_t>(p->n),
                                      p->max_elems, st));
       g_launches.fetch_add(1);
       extra = 1;
+      if (cert) {
+        QT_CUDA(qt::launch_replay3(p->kind, a, static_cast<uint32_t>(p->sm_count) * 4u, st));
+        g_launches.fetch_add(1);
+        extra = 2;
+      }
     } else if (p->d_chdr && cell_enabled()) {  // d >= 2: exact cell-list search
       qt::Alg3CellArgs ca{a, p->d_chdr, p->d_cstart, p->d_clist};
       QT_CUDA(qt::launch_alg3_cell(p->kind, src, ca, static_cast<uint32_t>(slices), st));

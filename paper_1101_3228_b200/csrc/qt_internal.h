@@ -136,6 +136,14 @@ struct Alg3Args {
   uint32_t buf_bytes;
   uint32_t probe_nored;   // diagnostics only (QT_PROBE_NORED): skip the count REDs
   const uint8_t* xtables;  // k_alg3_x: threshold-pair tables (see PathArgs::xtables)
+  // k_alg3_x<CERT>: uncertified samples (key = unit << 16 | k) for k_replay3, the
+  // original-index counts they and an overflowing list are replayed into, and
+  // (J^2)^-1 (the state after a sample's pair -> the state before it)
+  AmbEntry* amb;
+  unsigned long long* stats;
+  uint64_t amb_cap;
+  unsigned long long* ojoint;
+  uint32_t back2[18];
 };
 
 // d >= 2 cell-list path kernels (qt_cell.cu): exact tables (FP64 points) and
@@ -205,6 +213,7 @@ cudaError_t launch_sum_u64(const unsigned long long* v, uint64_t n, unsigned lon
 cudaError_t launch_paths_x(int kind, bool resident, int P, bool cert, const PathArgs& a,
                            uint32_t blocks, size_t smem, cudaStream_t st, int* bps);
 cudaError_t launch_replay(int kind, const FastArgs& f, uint32_t blocks, cudaStream_t st);
+cudaError_t launch_replay3(int kind, const Alg3Args& a, uint32_t blocks, cudaStream_t st);
 cudaError_t launch_apx_bounds_check(unsigned long long* out, cudaStream_t st);
 // joint[t][orig_t[a] N_{t+1} + orig_{t+1}[b]] += sjoint[t][a N_{t+1} + b] for every
 // layer t (sorted-cell counts of k_paths_x -> the reference's original indices);
@@ -242,8 +251,8 @@ cudaError_t launch_nearest_scan(int dim, const uint8_t* stable, uint32_t sbytes,
                                 unsigned long long* out, cudaStream_t st);
 cudaError_t launch_alg3(int kind, int src, const Alg3Args& a, uint32_t slices, size_t smem,
                         cudaStream_t st);
-cudaError_t launch_alg3_x(int kind, int P, const Alg3Args& a, uint32_t slices, size_t smem,
-                          cudaStream_t st);
+cudaError_t launch_alg3_x(int kind, int P, bool cert, const Alg3Args& a, uint32_t slices,
+                          size_t smem, cudaStream_t st);
 cudaError_t launch_gmem(int kind, int src, bool alg3, const PathArgs& pa, const Alg3Args& aa,
                         uint32_t blocks, cudaStream_t st);
 cudaError_t launch_finalize(bool alg3, const unsigned long long* joint, unsigned long long* visits,

@@ -895,7 +895,65 @@ __global__ void __launch_bounds__(kThreads) k_alg3(const Alg3Args a) {
 // slice) so the P dependency chains interleave. Tables k-1 and k stay in
 // shared memory for the CTA's lifetime.
 // ---------------------------------------------------------------------------
-template <int K, int P>
+// Exact replay of one uncertified Alg III sample (k_alg3's arithmetic, exact
+// tables in global memory) into the original-index counts a.ojoint.
+template <int K>
+__device__ __noinline__ void replay3_entry(const Alg3Args& a, const AmbEntry& ent) {
+  using C = Chain<K>;
+  Source<kSrcMrg> src;
+  src.s = Mrg{ent.st[0], ent.st[1], ent.st[2], ent.st[3], ent.st[4], ent.st[5]};
+  src.has = false;
+  const uint32_t k = static_cast<uint32_t>(ent.key & 0xFFFFu);
+  const uint8_t* tk = a.tables + __ldg(a.tab_off + k - 1);
+  const LayerTable& hk = *reinterpret_cast<const LayerTable*>(tk);
+  double e[2], x[1], xn[1];
+  e[0] = src.normal();
+  e[1] = src.normal();
+  C::marginal(hk.marg_prev, k == 1, x, e);
+  C::step(hk.step, x, xn, e + 1);
+  uint32_t i = 0;
+  if (k >= 2) {
+    const uint8_t* tp = a.tables + __ldg(a.tab_off + k - 2);
+    i = nearest_1d(*reinterpret_cast<const LayerTable*>(tp), tp, x[0], a.tables);
+  }
+  const uint32_t j = nearest_1d(hk, tk, xn[0], a.tables);
+  red_add_u64(a.ojoint + hk.joff + static_cast<uint64_t>(i) * hk.n_pts + j, 1ull);
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) k_replay3(const __grid_constant__ Alg3Args a) {
+  const unsigned long long entries = *reinterpret_cast<volatile unsigned long long*>(a.stats);
+  const uint64_t n = entries < a.amb_cap ? entries : a.amb_cap;
+  const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g0 == 0) atomicAdd(a.stats + 1, static_cast<unsigned long long>(n));
+  for (uint64_t g = g0; g < n; g += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    replay3_entry<K>(a, a.amb[g]);
+}
+
+cudaError_t launch_replay3(int kind, const Alg3Args& a, uint32_t blocks, cudaStream_t st) {
+  if (kind == 0) k_replay3<0><<<blocks, 256, 0, st>>>(a);
+  else k_replay3<2><<<blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// The cell of every state in [x - e, x + e] on an x-table, if there is one
+// (the certificate of k_paths_x<CERT>, for a single query).
+__device__ __forceinline__ bool cert_cell(const LayerTable& h, const uint8_t* tb, double x, float e,
+                                          uint32_t& j) {
+  const double ed = static_cast<double>(e);
+  const double xl = __dsub_rd(x, ed), xh = __dadd_ru(x, ed);
+  const bool safe = __dadd_ru(fabs(x), ed) < static_cast<double>(h.cert_xmax);
+  const uint16_t* start = reinterpret_cast<const uint16_t*>(tb + h.off_start);
+  const double2* PT = reinterpret_cast<const double2*>(tb + h.off_rec);
+  const uint32_t c = start[bucket_of(safe ? xl : 0.0, h.lo, h.inv_w, h.nb_d, h.nb)];
+  const double2 r = PT[c];
+  const bool in0 = xh < r.x;
+  const bool in1 = !(xl < r.x) && xh < r.y;
+  j = in0 ? c : c + 1;
+  return safe && (in0 || in1);
+}
+
+template <int K, int P, bool CERT>
 __global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg3Args a) {
   using C = Chain<K>;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -922,19 +980,24 @@ __global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg
   mbar_wait(&bar, 0);
   const LayerTable& hk = *reinterpret_cast<const LayerTable*>(tk);
   const LayerTable& hp = *reinterpret_cast<const LayerTable*>(tp);
+  // CERT: the marginal sample x = RN(m z1) is within fm b1 (1 + 2^-50) + cx of the
+  // exact one (|z1| <= 6.7 for every MRG32k3a uniform bounds the rounding term)
+  const float fm = __double2float_ru(fabs(hk.marg_prev[0]));
+  const float cx = __fmul_ru(__fmul_ru(fm, 6.7f), 0x1p-50f);
   // the slice split over blockDim.x * P slots, slot v = tid * P + p
   const uint64_t len = hi - lo, T = static_cast<uint64_t>(blockDim.x) * P;
   const uint64_t q = len / T, rem = len % T;
   Mrg st[P];
-  uint64_t cnt[P];
+  uint64_t cnt[P], beg[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     const uint64_t v = static_cast<uint64_t>(tid) * P + p;
     cnt[p] = q + (v < rem ? 1u : 0u);
+    beg[p] = lo + v * q + (v < rem ? v : rem);
     st[p] = Mrg{};
     if (cnt[p]) {
       Source<kSrcMrg> src;
-      src.start(a.src, lo + v * q + (v < rem ? v : rem));
+      src.start(a.src, beg[p]);
       st[p] = src.s;
     }
   }
@@ -943,6 +1006,7 @@ __global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg
   const uint32_t npts = hk.n_pts;
   for (uint64_t r = 0; r < rounds; ++r) {
     double z1[P], z2[P], v1[P], v2[P];
+    float b[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       uint32_t u1, u2;
@@ -950,15 +1014,60 @@ __global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg
       v1[p] = mrg_to_unit(u1);
       v2[p] = mrg_to_unit(u2);
     }
-    box_muller_batch<P>(v1, v2, z1, z2);
+    if constexpr (CERT) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const double rr = apx::radius(v1[p]);
+        double sn, cs;
+        apx::sincos(__dmul_rn(kTwoPi, v2[p]), &sn, &cs);
+        z1[p] = __dmul_rn(rr, cs);
+        z2[p] = __dmul_rn(rr, sn);
+        b[p] = __double2float_ru(__dmul_ru(rr, apx::kApxZ));
+      }
+    } else {
+      box_muller_batch<P>(v1, v2, z1, z2);
+    }
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       double e0[1] = {z1[p]}, e1[1] = {z2[p]}, x[1], xn[1];
       C::marginal(hk.marg_prev, k == 1, x, e0);  // sample_marginal(k-1, ...)
       C::step(hk.step, x, xn, e1);               // step(k-1, ...)
-      const uint32_t i = k == 1 ? 0u : nearest_1d_pos(hp, tp, x[0], a.tables);
-      const uint32_t j = nearest_1d_pos(hk, tk, xn[0], a.tables);
-      if (r < cnt[p] && !a.probe_nored) red_add_u64(jl + static_cast<uint64_t>(i) * npts + j, 1ull);
+      if constexpr (CERT) {
+        const float ex = k == 1 ? 0.0f : __fadd_ru(__fmaf_ru(__fmul_ru(fm, b[p]), 0x1p-50f,
+                                                             __fmul_ru(fm, b[p])), cx);
+        const float lin = __fmaf_ru(hk.fa, ex, __fmul_ru(hk.fs, b[p]));
+        const float exn = __fadd_ru(__fmaf_ru(lin, 0x1p-50f, lin), hk.cert_c);
+        uint32_t i = 0, j;
+        const bool oki = k == 1 || cert_cell(hp, tp, x[0], ex, i);
+        const bool okj = cert_cell(hk, tk, xn[0], exn, j);
+        if (r < cnt[p]) {
+          if (oki && okj) {
+            if (!a.probe_nored) red_add_u64(jl + static_cast<uint64_t>(i) * npts + j, 1ull);
+          } else {  // the sample's start state -> the replay list (or inline when full)
+            Mrg s0 = st[p];
+            mrg_apply(a.back2, s0);
+            AmbEntry ent;
+            ent.key = ((beg[p] + r) << 16) | k;
+            ent.st[0] = s0.a0;
+            ent.st[1] = s0.a1;
+            ent.st[2] = s0.a2;
+            ent.st[3] = s0.b0;
+            ent.st[4] = s0.b1;
+            ent.st[5] = s0.b2;
+            const unsigned long long idx = atomicAdd(a.stats, 1ull);
+            if (idx < a.amb_cap) {
+              a.amb[idx] = ent;
+            } else {
+              replay3_entry<K>(a, ent);
+              atomicAdd(a.stats + 2, 1ull);
+            }
+          }
+        }
+      } else {
+        const uint32_t i = k == 1 ? 0u : nearest_1d_pos(hp, tp, x[0], a.tables);
+        const uint32_t j = nearest_1d_pos(hk, tk, xn[0], a.tables);
+        if (r < cnt[p] && !a.probe_nored) red_add_u64(jl + static_cast<uint64_t>(i) * npts + j, 1ull);
+      }
     }
   }
 }
@@ -1389,8 +1498,8 @@ cudaError_t launch_alg3(int kind, int src, const Alg3Args& a, uint32_t slices, s
 }
 
 // k_alg3_x (kind 0 = Brownian, 2 = OU; MRG32k3a), P samples in flight per thread
-cudaError_t launch_alg3_x(int kind, int P, const Alg3Args& a, uint32_t slices, size_t smem,
-                          cudaStream_t st) {
+cudaError_t launch_alg3_x(int kind, int P, bool cert, const Alg3Args& a, uint32_t slices,
+                          size_t smem, cudaStream_t st) {
   const dim3 g(slices, a.n);
   auto go = [&](auto fn) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1399,8 +1508,13 @@ cudaError_t launch_alg3_x(int kind, int P, const Alg3Args& a, uint32_t slices, s
     fn<<<g, kThreads, smem, st>>>(a);
     return cudaGetLastError();
   };
-  if (kind == 0) return P == 1 ? go(k_alg3_x<0, 1>) : P == 4 ? go(k_alg3_x<0, 4>) : go(k_alg3_x<0, 2>);
-  return P == 1 ? go(k_alg3_x<2, 1>) : P == 4 ? go(k_alg3_x<2, 4>) : go(k_alg3_x<2, 2>);
+  if (cert) {
+    if (kind == 0) return P == 1 ? go(k_alg3_x<0, 1, true>) : go(k_alg3_x<0, 2, true>);
+    return P == 1 ? go(k_alg3_x<2, 1, true>) : go(k_alg3_x<2, 2, true>);
+  }
+  if (kind == 0)
+    return P == 1 ? go(k_alg3_x<0, 1, false>) : P == 4 ? go(k_alg3_x<0, 4, false>) : go(k_alg3_x<0, 2, false>);
+  return P == 1 ? go(k_alg3_x<2, 1, false>) : P == 4 ? go(k_alg3_x<2, 4, false>) : go(k_alg3_x<2, 2, false>);
 }
 
 cudaError_t launch_finalize(bool alg3, const unsigned long long* joint, unsigned long long* visits,

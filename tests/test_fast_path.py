@@ -221,3 +221,41 @@ def test_certified_fp64_replays_adversarial(gpu):
     cert = _counts(plan, 200000, 0, None, 2)
     exact = _counts(plan, 200000, 0, None, False)
     assert np.array_equal(cert, exact)
+
+
+def _counts3(plan, M, n, mode):
+    import torch
+    q = Q()
+    q.set_fast_path(mode)
+    try:
+        joint = plan.zeros_joint()
+        plan.count(2, 1, 4242, 0, M * n, M * n, joint)
+        torch.cuda.synchronize()
+        return joint.cpu().numpy().view(np.uint64).copy()
+    finally:
+        q.set_fast_path(True)
+
+
+@pytest.mark.parametrize("case", ["c3", "adversarial"])
+def test_certified_alg3_equals_exact(gpu, case):
+    """Alg III (k_alg3_x) certified with the approximate FP64 pair equals the
+    exact kernel: on the C3 OU chain (no sample needs the replay) and on grids
+    of 3e-14-wide cell pairs (most samples replayed by k_replay3)."""
+    from paper_1101_3228_b200.device import Plan
+    q = Q()
+    n = 40 if case == "c3" else 6
+    p = q.TwoFactorParams(sigma1=0.5, alpha1=1.0, sigma2=0.0, steps=n)
+    ch = q.OuChain1d(p)
+    if case == "c3":
+        grids = q.build_ou_grids(ch, 200)
+    else:
+        rng = np.random.default_rng(9)
+        grids = []
+        for k in range(1, n + 1):
+            base = np.sort(rng.standard_normal(30)) * 0.4
+            grids.append(q.QuantGrid(1, np.concatenate([base, base + 3e-14 * (1 + np.abs(base))])))
+    plan = Plan(ch, grids, 0)
+    M = 200000 if case == "c3" else 30000
+    cert = _counts3(plan, M, n, 2)
+    exact = _counts3(plan, M, n, False)
+    assert np.array_equal(cert, exact), case
