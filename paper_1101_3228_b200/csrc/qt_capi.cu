@@ -1759,9 +1759,15 @@ void run_estimate(int alg, const qt_chain* chain, const qt_grids* grids, uint64_
       QT_CUDA(cudaMemcpyAsync(hv.data(), d_vis, p0->nvis * 8, cudaMemcpyDeviceToHost, streams[0]));
       QT_CUDA(cudaMemcpyAsync(hj.data(), dj[0], p0->njoint * 8, cudaMemcpyDeviceToHost, streams[0]));
     } else if (!keep) {
+      if (dbg) {
+        QT_CUDA(cudaStreamSynchronize(streams[0]));
+        mark("kernels done");
+      }
       prefault.join();
+      mark("prefaulted");
       d2h_pinned(visits, d_vis, p0->nvis * 8, streams[0]);
       d2h_pinned(joint, dj[0], p0->njoint * 8, streams[0]);
+      mark("joint d2h");
       if (pi) d2h_pinned(pi, d_pi, p0->njoint * 8, streams[0]);
     }
     QT_CUDA(cudaStreamSynchronize(streams[0]));

@@ -1,21 +1,17 @@
-"""Phase timing of the one-call estimate (QT_DEBUG marks) for C1 / C2 shapes.
-
-    QT_DEBUG=1 python tools/e2e_probe.py [c1|c2] [paths]
-"""
-import os
-import sys
-import time
-
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_1101_3228_b200 import qtree as Q  # noqa: E402
-
-cfg = sys.argv[1] if len(sys.argv) > 1 else "c1"
-n, N, M = {"c1": (10, 100, 10**6), "c2": (50, 500, 10**9)}[cfg]
-if len(sys.argv) > 2:
-    M = int(float(sys.argv[2]))
-ch = Q.BrownianChain1d(n)
-grids = Q.build_brownian_grids(ch, N)
-for it in range(4):
-    t0 = time.perf_counter()
-    t = Q.estimate(1, ch, grids, M)
-    print(f"call {it}: {(time.perf_counter() - t0) * 1e3:.2f} ms", file=sys.stderr, flush=True)
+import sys, time
+sys.path.insert(0, ".")
+import torch
+from paper_1101_3228_b200 import qtree as q
+from paper_1101_3228_b200.device import Plan
+ch = q.BrownianChain1d(50); g = q.build_brownian_grids(ch, 500)
+M = 10**9
+plan = Plan(ch, g, 0)
+joint = plan.zeros_joint()
+for i in range(3):
+    joint.zero_(); torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(); plan.count(1, 1, 12345, 0, M, M, joint); e1.record(); torch.cuda.synchronize()
+    print("plan.count", e0.elapsed_time(e1), flush=True)
+q.estimate_alg2(ch, g, M)
+for i in range(2):
+    t = time.perf_counter(); r = q.estimate_alg2(ch, g, M); print("one-call", time.perf_counter() - t, flush=True)
