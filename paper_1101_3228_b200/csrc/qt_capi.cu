@@ -1382,7 +1382,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
     slices = std::min<uint64_t>(slices, 1u << 30);
     if (src == QT_ENGINE_MRG32K3A && (p->kind == QT_CHAIN_BROWNIAN_1D || p->kind == QT_CHAIN_OU_1D) &&
         xkernel_enabled() && !p->gmem && p->d_xtables) {
-      int P = 1;  // measured best for C3 (tools/alg3_probe.py)
+      int P = 1;  // measured best for C3 (exact: P = 1; certified: P = 1 8.24e10 vs P = 2 7.93e10)
       if (const char* e = std::getenv("QT_X_P")) P = std::atoi(e) == 2 ? 2 : std::atoi(e) == 4 ? 4 : 1;
       // sorted-cell counts into the plan's scratch, then permute-added (as k_paths_x)
       if (!p->d_sjoint) QT_CUDA(cudaMalloc(&p->d_sjoint, p->njoint * sizeof(uint64_t)));
