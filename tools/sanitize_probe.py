@@ -3,7 +3,7 @@
     compute-sanitizer --tool memcheck python tools/sanitize_probe.py
     compute-sanitizer --tool racecheck python tools/sanitize_probe.py
 
-Covers the default kernels (certified 1-D fast path + replay, the cell-list
+Covers the default kernels (certified 1-D paths and Alg III + replays, the cell-list
 d >= 2 search and its device-built index, the Alg III samplers), the
 selectable alternatives (exact k_paths_x, the FP32 scan), the estimate ->
 price path on the device tree, and the GPU Lloyd.
@@ -18,10 +18,10 @@ from paper_1101_3228_b200 import qtree as Q  # noqa: E402
 def run_all():
     ch = Q.BrownianChain1d(10)
     g = Q.build_brownian_grids(ch, 100)                     # GPU Lloyd (k_serial_normals, ...)
-    Q.estimate_alg2(ch, g, 20000)                           # k_paths_fast + k_replay (resident)
+    Q.estimate_alg2(ch, g, 20000)                           # 1-D path kernel (resident tables)
     ch50 = Q.BrownianChain1d(50)
     g50 = Q.build_brownian_grids(ch50, 500)
-    Q.estimate_alg2(ch50, g50, 20000)                       # k_paths_fast (staged), permute-add
+    Q.estimate_alg2(ch50, g50, 20000)                       # 1-D path kernel (staged), permute-add
     ou = Q.OuChain1d(Q.TwoFactorParams(sigma1=0.5, alpha1=1.0, sigma2=0.0, steps=12))
     go = Q.build_ou_grids(ou, 50)
     Q.estimate_alg3(ou, go, 4000)                           # k_alg3_x
@@ -37,9 +37,10 @@ def run_all():
         Q.solve_stopping(dt, Q.make_put_payoff(Q.TwoFactorParams(steps=6), 2))
 
 
-run_all()
-os.environ["QT_FAST_PATH"] = "0"
-Q.set_fast_path(False)
+run_all()                                                   # certified k_paths_x / k_alg3_x + replays
+Q.set_fast_path(1)
+run_all()                                                   # FP32 k_paths_fast + k_replay
+Q.set_fast_path(0)
 os.environ["QT_NN"] = "scan"
-run_all()                                                   # k_paths_x, k_paths_scan, k_alg3_scan
+run_all()                                                   # exact k_paths_x / k_alg3_x, FP32 scans
 print("sanitize probe ok")
