@@ -803,6 +803,7 @@ struct qt_plan {
   qt::CellHdr* d_chdr = nullptr;  // cell-list index (d >= 2, qt_cell.cu): headers [n],
   uint32_t* d_cstart = nullptr;   // bucket starts over all layers, and
   uint16_t* d_clist = nullptr;    // the candidate lists
+  uint4* d_crec = nullptr;        // bucket records (short lists inline)
   uint32_t* d_stab_off = nullptr;
   uint32_t* d_stab_bytes = nullptr;
   uint32_t max_stab = 0, total_stab = 0;
@@ -846,6 +847,7 @@ struct qt_plan {
     cudaFree(d_chdr);
     cudaFree(d_cstart);
     cudaFree(d_clist);
+    cudaFree(d_crec);
     cudaFree(d_stab_off);
     cudaFree(d_stab_bytes);
     cudaFree(d_ftab_off);
@@ -1050,8 +1052,14 @@ qt_plan* make_plan(const qt_chain* chain, const qt_grids* grids, int device) {
       pts_off[k - 1] = p->tab_off[k - 1] + lt.off_rec;
     }
     uint64_t total = 0;
+    // inline bucket records: d = 2 lists are short (C4: <= 6 candidates) and the
+    // record saves one dependent load (C4 3.0e10 vs 2.33e10); d = 3 lists mostly
+    // overflow the 7 slots (C5 5.37e9 vs 5.55e9 without). QT_CELL_REC=0/1 overrides.
+    bool recs = p->dim == 2;
+    if (const char* e = std::getenv("QT_CELL_REC")) recs = e[0] != '0';
     QT_CUDA(qt::build_cell_lists(p->dim, n, chdr.data(), p->sizes.data() + 1, p->d_tables,
-                                 pts_off.data(), &p->d_chdr, &p->d_cstart, &p->d_clist, &total));
+                                 pts_off.data(), &p->d_chdr, &p->d_cstart, &p->d_clist,
+                                 recs ? &p->d_crec : nullptr, &total));
     g_launches.fetch_add(2ull * n + 1);
   }
   std::vector<uint64_t> fin(5 * n);
@@ -1307,7 +1315,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       const uint64_t cneed = (count + per_block - 1) / per_block;
       if (cneed < cblocks) cblocks = cneed;
       const uint64_t T = cblocks * per_block;
-      qt::CellArgs ca{a, p->d_chdr, p->d_cstart, p->d_clist};
+      qt::CellArgs ca{a, p->d_chdr, p->d_cstart, p->d_clist, p->d_crec};
       ca.p.q = count / T;
       ca.p.rem = count % T;
       QT_CUDA(qt::launch_paths_cell(p->kind, src, P, ca, static_cast<uint32_t>(cblocks), st));
@@ -1423,7 +1431,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
         extra = 2;
       }
     } else if (p->d_chdr && cell_enabled()) {  // d >= 2: exact cell-list search
-      qt::Alg3CellArgs ca{a, p->d_chdr, p->d_cstart, p->d_clist};
+      qt::Alg3CellArgs ca{a, p->d_chdr, p->d_cstart, p->d_clist, p->d_crec};
       QT_CUDA(qt::launch_alg3_cell(p->kind, src, ca, static_cast<uint32_t>(slices), st));
     } else if (p->d_stables && scan_enabled() && 2ull * p->max_stab <= 200u * 1024u) {
       qt::Alg3ScanArgs sa{a, p->d_stables, p->d_stab_off, p->d_stab_bytes, p->max_stab};

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cub/cub.cuh>
 #include <vector>
 
@@ -57,10 +58,13 @@ __device__ __forceinline__ double cell_d2(const double* P, uint32_t idx, const d
 }
 
 // The reference's nearest index of q on one layer (see the file header).
+// With bucket records (crec), the candidates of most buckets come with the
+// record itself: one dependent L2 load fewer per query.
 template <int D>
 __device__ __forceinline__ uint32_t cell_nearest(const CellHdr* hp, const uint32_t* cstart,
-                                                 const uint16_t* clist, const uint8_t* xb,
-                                                 const double (&q)[D], const uint8_t* gtables) {
+                                                 const uint16_t* clist, const uint4* crec,
+                                                 const uint8_t* xb, const double (&q)[D],
+                                                 const uint8_t* gtables) {
   const LayerTable& hx = *reinterpret_cast<const LayerTable*>(xb);
   bool in = __ldg(&hp->ok) != 0;
   uint32_t b = 0;
@@ -75,7 +79,33 @@ __device__ __forceinline__ uint32_t cell_nearest(const CellHdr* hp, const uint32
   if (!in) return nearest<D>(hx, xb, q, gtables);  // exact full scan (nn.hpp:18-46)
   const uint64_t sb = __ldg(reinterpret_cast<const unsigned long long*>(&hp->start_off)) + b;
   const double* P = reinterpret_cast<const double*>(xb + hx.off_rec);
-  const uint32_t s = __ldg(cstart + sb), e = __ldg(cstart + sb + 1);
+  uint32_t s, e;
+  if (crec) {
+    const uint4 rr = __ldg(crec + sb);
+    const uint32_t n = rr.x & 0xFFFFu;
+    if (n != 0xFFFFu) {  // inline: n <= 7 candidates, ascending
+      const uint32_t c[7] = {rr.x >> 16, rr.y & 0xFFFFu, rr.y >> 16, rr.z & 0xFFFFu, rr.z >> 16,
+                             rr.w & 0xFFFFu, rr.w >> 16};
+      uint32_t best = c[0];
+      double bd = cell_d2<D>(P, best, q);
+#pragma unroll
+      for (uint32_t u = 1; u < 7; ++u) {
+        if (u < n) {
+          const double d = cell_d2<D>(P, c[u], q);
+          if (d < bd) {
+            bd = d;
+            best = c[u];
+          }
+        }
+      }
+      return best;
+    }
+    s = rr.y;
+    e = rr.y + rr.z;
+  } else {
+    s = __ldg(cstart + sb);
+    e = __ldg(cstart + sb + 1);
+  }
   uint32_t best = __ldg(clist + s);
   double bd = cell_d2<D>(P, best, q);
   for (uint32_t u = s + 1; u < e; ++u) {
@@ -87,6 +117,25 @@ __device__ __forceinline__ uint32_t cell_nearest(const CellHdr* hp, const uint32
     }
   }
   return best;
+}
+
+// bucket records from start[] / list[] (see CellArgs::crec), one thread per bucket
+__global__ void k_cell_records(uint64_t nb_all, const uint32_t* start, const uint16_t* list,
+                               uint4* rec) {
+  for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < nb_all;
+       b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t s = start[b], n = start[b + 1] - s;
+    uint4 r;
+    if (n <= 7 && n > 0) {
+      uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (uint32_t u = 0; u < n; ++u) c[u + 1] = list[s + u];
+      c[0] = n;
+      r = make_uint4(c[0] | (c[1] << 16), c[2] | (c[3] << 16), c[4] | (c[5] << 16), c[6] | (c[7] << 16));
+    } else {
+      r = make_uint4(0xFFFFu, s, n, 0u);
+    }
+    rec[b] = r;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -191,7 +240,8 @@ __global__ void __launch_bounds__(256) k_cell_fill(const CellHdr h, const double
 
 cudaError_t build_cell_lists(int dim, int n, const CellHdr* hdr, const uint64_t* npts,
                              const uint8_t* tables, const uint64_t* pts_off, CellHdr** d_hdr,
-                             uint32_t** d_start, uint16_t** d_list, uint64_t* total) {
+                             uint32_t** d_start, uint16_t** d_list, uint4** d_rec,
+                             uint64_t* total) {
   uint64_t nb_all = 0;
   for (int k = 0; k < n; ++k) nb_all += static_cast<uint64_t>(hdr[k].g[0]) * hdr[k].g[1] * hdr[k].g[2];
   uint32_t* counts = nullptr;
@@ -227,6 +277,14 @@ cudaError_t build_cell_lists(int dim, int n, const CellHdr* hdr, const uint64_t*
     if (dim == 2) k_cell_fill<2><<<grid(nb), 256>>>(hdr[k], P, N, *d_start, *d_list);
     else k_cell_fill<3><<<grid(nb), 256>>>(hdr[k], P, N, *d_start, *d_list);
     e = cudaGetLastError();
+  }
+  if (e == cudaSuccess && d_rec) {
+    e = cudaMalloc(d_rec, (nb_all ? nb_all : 1) * sizeof(uint4));
+    if (e == cudaSuccess) {
+      k_cell_records<<<static_cast<uint32_t>(std::min<uint64_t>((nb_all + 255) / 256, 148 * 64)), 256>>>(
+          nb_all, *d_start, *d_list, *d_rec);
+      e = cudaGetLastError();
+    }
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   cudaFree(counts);
@@ -286,7 +344,7 @@ __global__ void __launch_bounds__(kCellThreads, QT_CELL_MINB) k_paths_cell(const
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         if (r < cnt[p]) {
-          const uint32_t j = cell_nearest<D>(ch, f.cstart, f.clist, xb, x[p], a.tables);
+          const uint32_t j = cell_nearest<D>(ch, f.cstart, f.clist, f.crec, xb, x[p], a.tables);
           if (!a.probe_nored) red_add_u64(a.joint + joff + static_cast<uint64_t>(i[p]) * npts + j, 1ull);
           i[p] = j;
         }
@@ -337,8 +395,8 @@ __global__ void __launch_bounds__(kCellThreads) k_alg3_cell(const __grid_constan
     for (int q2 = 0; q2 < D + C::NPS; ++q2) e[q2] = src.normal();
     C::marginal(mg, k == 1, x, e);  // sample_marginal(k-1, ...)
     C::step(stp, x, xn, e + D);      // step(k-1, ...)
-    const uint32_t j = cell_nearest<D>(ck, f.cstart, f.clist, xk, xn, a.tables);
-    const uint32_t i = k >= 2 ? cell_nearest<D>(cp, f.cstart, f.clist, xp, x, a.tables) : 0u;
+    const uint32_t j = cell_nearest<D>(ck, f.cstart, f.clist, f.crec, xk, xn, a.tables);
+    const uint32_t i = k >= 2 ? cell_nearest<D>(cp, f.cstart, f.clist, f.crec, xp, x, a.tables) : 0u;
     if (!a.probe_nored) red_add_u64(jl + static_cast<uint64_t>(i) * npts + j, 1ull);
   }
 }

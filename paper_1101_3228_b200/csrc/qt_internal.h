@@ -153,19 +153,23 @@ struct CellArgs {
   const CellHdr* chdr;        // [n] layer k's header at index k-1
   const uint32_t* cstart;     // bucket list starts, all layers (+ a final end)
   const uint16_t* clist;      // candidate point indices, ascending per bucket
+  const uint4* crec;          // per bucket: up to 7 candidates inline (x: n | c0 << 16,
+                              // y..w: c1..c6), or n = 0xFFFF: y = list start, z = count
 };
 struct Alg3CellArgs {
   Alg3Args a;
   const CellHdr* chdr;
   const uint32_t* cstart;
   const uint16_t* clist;
+  const uint4* crec;
 };
 // Builds the cell lists of n layers on the current device (synchronous):
 // hdr[n] (host) geometry with start_off set, npts[n] = N_k, the FP64 points of
 // layer k at tables + pts_off[k-1]. Allocates *d_hdr, *d_start, *d_list.
 cudaError_t build_cell_lists(int dim, int n, const CellHdr* hdr, const uint64_t* npts,
                              const uint8_t* tables, const uint64_t* pts_off, CellHdr** d_hdr,
-                             uint32_t** d_start, uint16_t** d_list, uint64_t* total);
+                             uint32_t** d_start, uint16_t** d_list, uint4** d_rec,
+                             uint64_t* total);
 
 struct FinalizeArgs {
   const uint64_t* rows;      // [n] N_{t}
