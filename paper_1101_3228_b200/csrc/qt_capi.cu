@@ -579,7 +579,7 @@ qt::CellHdr cell_geometry(int dim, uint64_t N, const double* pts) {
       mx[c] = std::max(mx[c], v);
     }
   }
-  double per = dim == 2 ? 6.0 : 5.0;
+  double per = 6.0;  // d = 3: 6 measured 5.87e9 at C5 (5: 5.56e9, 7: 5.90e9 with a larger index)
   if (const char* e = std::getenv(dim == 2 ? "QT_CELL_G2" : "QT_CELL_G3")) per = std::atof(e);
   const uint32_t gax = static_cast<uint32_t>(
       std::min(dim == 2 ? 1024.0 : 96.0, std::max(1.0, std::round(per * std::pow(double(N), 1.0 / dim)))));
