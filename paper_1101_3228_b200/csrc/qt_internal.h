@@ -144,6 +144,9 @@ struct Alg3Args {
   uint64_t amb_cap;
   unsigned long long* ojoint;
   uint32_t back2[18];
+  // k_alg3_x<PRIV>: bytes of the CTA's shared-memory count tile (n_{k-1} x n_k
+  // u32 counters after the two table buffers), flushed to `joint` at the end
+  uint32_t priv_bytes;
 };
 
 // d >= 2 cell-list path kernels (qt_cell.cu): exact tables (FP64 points) and

@@ -953,8 +953,11 @@ __device__ __forceinline__ bool cert_cell(const LayerTable& h, const uint8_t* tb
   return safe && (in0 || in1);
 }
 
-template <int K, int P, bool CERT>
-__global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg3Args a) {
+// PRIV: the layer's counts privatised in a shared-memory tile (one CTA = one
+// slice of one layer, 1024 threads, one CTA per SM) and flushed once per CTA
+// with one RED per non-zero cell; otherwise one L2 RED per sample.
+template <int K, int P, bool CERT, bool PRIV>
+__global__ void __launch_bounds__(PRIV ? 1024 : kThreads) k_alg3_x(const __grid_constant__ Alg3Args a) {
   using C = Chain<K>;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar;
@@ -968,6 +971,10 @@ __global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg
   if (lo >= hi) return;
   const uint8_t* tk = smem;
   const uint8_t* tp = smem + a.buf_bytes;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + 2ull * a.buf_bytes);
+  if constexpr (PRIV) {
+    for (uint32_t c = tid; c < a.priv_bytes / 4; c += blockDim.x) hist[c] = 0u;
+  }
   if (tid == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
@@ -1042,7 +1049,8 @@ __global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg
         const bool okj = cert_cell(hk, tk, xn[0], exn, j);
         if (r < cnt[p]) {
           if (oki && okj) {
-            if (!a.probe_nored) red_add_u64(jl + static_cast<uint64_t>(i) * npts + j, 1ull);
+            if constexpr (PRIV) atomicAdd(hist + i * npts + j, 1u);
+            else if (!a.probe_nored) red_add_u64(jl + static_cast<uint64_t>(i) * npts + j, 1ull);
           } else {  // the sample's start state -> the replay list (or inline when full)
             Mrg s0 = st[p];
             mrg_apply(a.back2, s0);
@@ -1066,8 +1074,20 @@ __global__ void __launch_bounds__(kThreads) k_alg3_x(const __grid_constant__ Alg
       } else {
         const uint32_t i = k == 1 ? 0u : nearest_1d_pos(hp, tp, x[0], a.tables);
         const uint32_t j = nearest_1d_pos(hk, tk, xn[0], a.tables);
-        if (r < cnt[p] && !a.probe_nored) red_add_u64(jl + static_cast<uint64_t>(i) * npts + j, 1ull);
+        if constexpr (PRIV) {
+          if (r < cnt[p]) atomicAdd(hist + i * npts + j, 1u);
+        } else if (r < cnt[p] && !a.probe_nored) {
+          red_add_u64(jl + static_cast<uint64_t>(i) * npts + j, 1ull);
+        }
       }
+    }
+  }
+  if constexpr (PRIV) {  // flush the tile: one RED per non-zero cell
+    __syncthreads();
+    const uint32_t cells = (k == 1 ? 1u : hp.n_pts) * npts;
+    for (uint32_t c = tid; c < cells; c += blockDim.x) {
+      const uint32_t v = hist[c];
+      if (v) red_add_u64(jl + c, static_cast<unsigned long long>(v));
     }
   }
 }
@@ -1501,20 +1521,27 @@ cudaError_t launch_alg3(int kind, int src, const Alg3Args& a, uint32_t slices, s
 cudaError_t launch_alg3_x(int kind, int P, bool cert, const Alg3Args& a, uint32_t slices,
                           size_t smem, cudaStream_t st) {
   const dim3 g(slices, a.n);
+  const bool priv = a.priv_bytes != 0;
   auto go = [&](auto fn) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    fn<<<g, kThreads, smem, st>>>(a);
+    fn<<<g, priv ? 1024 : kThreads, smem, st>>>(a);
     return cudaGetLastError();
   };
+  if (priv) {
+    if (cert) return kind == 0 ? go(k_alg3_x<0, 1, true, true>) : go(k_alg3_x<2, 1, true, true>);
+    return kind == 0 ? go(k_alg3_x<0, 1, false, true>) : go(k_alg3_x<2, 1, false, true>);
+  }
   if (cert) {
-    if (kind == 0) return P == 1 ? go(k_alg3_x<0, 1, true>) : go(k_alg3_x<0, 2, true>);
-    return P == 1 ? go(k_alg3_x<2, 1, true>) : go(k_alg3_x<2, 2, true>);
+    if (kind == 0) return P == 1 ? go(k_alg3_x<0, 1, true, false>) : go(k_alg3_x<0, 2, true, false>);
+    return P == 1 ? go(k_alg3_x<2, 1, true, false>) : go(k_alg3_x<2, 2, true, false>);
   }
   if (kind == 0)
-    return P == 1 ? go(k_alg3_x<0, 1, false>) : P == 4 ? go(k_alg3_x<0, 4, false>) : go(k_alg3_x<0, 2, false>);
-  return P == 1 ? go(k_alg3_x<2, 1, false>) : P == 4 ? go(k_alg3_x<2, 4, false>) : go(k_alg3_x<2, 2, false>);
+    return P == 1 ? go(k_alg3_x<0, 1, false, false>) : P == 4 ? go(k_alg3_x<0, 4, false, false>)
+                                                      : go(k_alg3_x<0, 2, false, false>);
+  return P == 1 ? go(k_alg3_x<2, 1, false, false>) : P == 4 ? go(k_alg3_x<2, 4, false, false>)
+                                                    : go(k_alg3_x<2, 2, false, false>);
 }
 
 cudaError_t launch_finalize(bool alg3, const unsigned long long* joint, unsigned long long* visits,

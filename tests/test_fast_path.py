@@ -259,3 +259,22 @@ def test_certified_alg3_equals_exact(gpu, case):
     cert = _counts3(plan, M, n, 2)
     exact = _counts3(plan, M, n, False)
     assert np.array_equal(cert, exact), case
+
+
+@pytest.mark.parametrize("mode", [2, 0])
+def test_alg3_count_tile_equals_l2_reds(gpu, monkeypatch, mode):
+    """The default Alg III kernel counts into a per-CTA shared-memory tile and
+    flushes it once; QT_A3_PRIV=0 issues one L2 RED per sample. Same counts,
+    certified (mode 2) and exact (mode 0), with several slices per layer."""
+    from paper_1101_3228_b200.device import Plan
+    q = Q()
+    n = 12
+    ch = q.OuChain1d(q.TwoFactorParams(sigma1=0.5, alpha1=1.0, sigma2=0.0, steps=n))
+    plan = Plan(ch, q.build_ou_grids(ch, 200), 0)
+    M = 300000
+    monkeypatch.setenv("QT_A3_SLICES", "3")
+    tile = _counts3(plan, M, n, mode)
+    monkeypatch.setenv("QT_A3_PRIV", "0")
+    reds = _counts3(plan, M, n, mode)
+    assert tile.sum() == M * n
+    assert np.array_equal(tile, reds)
