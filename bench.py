@@ -505,9 +505,11 @@ def run_ours(args, rank, world, local_rank):
                      "kernel_ms": t_kern, "peak_source": peak_src,
                      "algorithmic_bytes": "16 B per transition (u64 counter read-modify-write)",
                      "binding_unit": (
-                         "d = 1: the count scatter's L2 atomic throughput (one 64-bit RED per "
-                         "transition; tools/red_probe.cu measures 1.3-1.9e11 REDs/s on this B200 "
-                         "for such patterns, profiles/r02_red_probe_*.txt)" if kind in ("bm", "ou")
+                         "d = 1: instruction issue (see roofline_issue; 1.43e11/s with the count "
+                         "REDs removed) with the count scatter's L2 atomic ceiling close behind "
+                         "(one 64-bit RED per transition; tools/red_probe.cu measures 1.3-1.9e11 "
+                         "REDs/s on this B200 for such patterns, profiles/r02_red_probe_*.txt)"
+                         if kind in ("bm", "ou")
                          else "d >= 2: load latency of the candidate-list gathers (ncu: "
                               "long-scoreboard stalls ~58 %, profiles/r02_ncu_kernels.md)") +
                          "; see DESIGN.md section 4"},
