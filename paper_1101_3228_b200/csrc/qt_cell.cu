@@ -33,6 +33,9 @@
 namespace qt {
 
 constexpr int kCellThreads = 256;
+#ifndef QT_CELL_U  // candidates gathered per batch in the list scan
+#define QT_CELL_U 4
+#endif
 #ifndef QT_CELL_MINB  // resident CTAs per SM the register allocation must allow
 #define QT_CELL_MINB 3  // the kernel is load-latency bound: warps in flight pay (C4 +24 %)
 #endif
@@ -108,10 +111,29 @@ __device__ __forceinline__ uint32_t cell_nearest(const CellHdr* hp, const uint32
   }
   uint32_t best = __ldg(clist + s);
   double bd = cell_d2<D>(P, best, q);
-  for (uint32_t u = s + 1; u < e; ++u) {
+  uint32_t u = s + 1;
+  // QT_CELL_U candidates per batch: their list entries and points are loaded
+  // before any is compared, so the dependent L2 gathers overlap; the compares
+  // stay in list (ascending index) order, so ties resolve as in the scan
+  for (; u + QT_CELL_U <= e; u += QT_CELL_U) {
+    uint32_t id[QT_CELL_U];
+    double d[QT_CELL_U];
+#pragma unroll
+    for (int t = 0; t < QT_CELL_U; ++t) id[t] = __ldg(clist + u + t);
+#pragma unroll
+    for (int t = 0; t < QT_CELL_U; ++t) d[t] = cell_d2<D>(P, id[t], q);
+#pragma unroll
+    for (int t = 0; t < QT_CELL_U; ++t) {
+      if (d[t] < bd) {  // strict <: the smallest index among ties (lists are ascending)
+        bd = d[t];
+        best = id[t];
+      }
+    }
+  }
+  for (; u < e; ++u) {
     const uint32_t idx = __ldg(clist + u);
     const double d = cell_d2<D>(P, idx, q);
-    if (d < bd) {  // strict <: the smallest index among ties (lists are ascending)
+    if (d < bd) {
       bd = d;
       best = idx;
     }
