@@ -46,10 +46,12 @@ CONFIGS = {
     # name: (workload text, chain kind, n, N, M, estimator)
     "c1": ("C1: 1-D Black-Scholes American put, n=10, N=100, M=1e6 paths", "bm", 10, 100, 10**6, 1),
     "c2": ("C2: 1-D Black-Scholes American put, n=50, N=500, M=1e9 paths", "bm", 50, 500, 10**9, 1),
-    "c3": ("C3: 1-D OU swing, Alg III pair sampling, n=365, N=200, M=1e7 per layer", "ou", 365, 200,
-           10**7, 2),
-    "c4": ("C4: 2-factor AR(1) gas swing, n=365, N=1000, M=1e7 paths", "tf", 365, 1000, 10**7, 1),
-    "c5": ("C5: 3-D GBM max-call, n=20, N=4000, M=1e6 paths", "gbm", 20, 4000, 10**6, 1),
+    # C3 / C4: BASELINE gives no M; SURVEY.md 8(d) proposes 1e8 (per layer) on the GPU.
+    # C5: BASELINE's M = 4e9 (8e10 transitions, ~6 s per step on one B200).
+    "c3": ("C3: 1-D OU swing, Alg III pair sampling, n=365, N=200, M=1e8 per layer", "ou", 365, 200,
+           10**8, 2),
+    "c4": ("C4: 2-factor AR(1) gas swing, n=365, N=1000, M=1e8 paths", "tf", 365, 1000, 10**8, 1),
+    "c5": ("C5: 3-D GBM max-call, n=20, N=4000, M=4e9 paths", "gbm", 20, 4000, 4 * 10**9, 1),
 }
 
 
@@ -101,8 +103,22 @@ def reference_price(cfg, M):
         if cfg == "c1" and M == 10**6:
             with np.load(os.path.join(g, "configs.npz")) as z:
                 return float(z["c1_put_price"])
+        if cfg in ("c3", "c4", "c5"):
+            with np.load(os.path.join(g, "prices.npz")) as z:
+                if int(z[f"{cfg}_M"]) == M:
+                    return float(z[f"{cfg}_price"])
     except (OSError, KeyError):
         return None
+    return None
+
+
+def golden_price_m(cfg):
+    """M of the reference's committed price for a config (tests/golden), or None."""
+    g = os.path.join(ROOT, "tests", "golden", "prices.npz")
+    if cfg in ("c3", "c4", "c5") and os.path.exists(g):
+        with np.load(g) as z:
+            if f"{cfg}_M" in z.files:
+                return int(z[f"{cfg}_M"])
     return None
 
 
@@ -461,6 +477,18 @@ def run_ours(args, rank, world, local_rank):
         if ref is not None:
             price_line["reference_price"] = ref
             price_line["rel_err_vs_reference"] = abs(res.price - ref) / abs(ref)
+        mg = golden_price_m(args.config)
+        if ref is None and mg is not None:
+            # the config's M has no reference price (the CPU reference would take
+            # hours): price the same chain and grids at the golden's M instead,
+            # against the reference's own price there
+            with Q.estimate_device(est, ch, grids, mg) as dtree:
+                rg = (Q.solve_swing(dtree, payoff, q[0], q[1]) if q
+                      else Q.solve_stopping(dtree, payoff))
+            refg = reference_price(args.config, mg)
+            price_line["parity_at_golden_M"] = {
+                "M": mg, "price": rg.price, "reference_price": refg,
+                "rel_err_vs_reference": abs(rg.price - refg) / abs(refg)}
         if kind == "bm":
             crr = crr_bermudan_put(100.0, 100.0, 0.05, 0.2, 1.0, n)
             price_line["crr_bermudan"] = crr
