@@ -8,11 +8,15 @@
 // resulting error of the path state, and counts a transition only when every
 // state within the bound falls in one cell -- otherwise the path is replayed
 // with the exact arithmetic (k_replay). So here: a table log (128-entry
-// reduction, degree-8 tail; ~15 operations) and a branch-free sincos (one
-// Cody-Waite reduction by pi/2, fdlibm kernels; ~25 operations), both within
-// a few ulp of glibc. The bounds kApxRadRel / kApxAng are verified over EVERY
-// MRG32k3a uniform against the glibc-exact qt_math.h (k_apx_bounds_check,
-// tests/test_fast_path.py).
+// reduction, degree-6 tail, one FMA + two additions for the result; ~12
+// operations) and a branch-free sincos (a two-part Cody-Waite reduction by
+// pi/2, the fdlibm polynomials without their tail corrections; ~20
+// operations): radius within 8.4e-15 relative and sin / cos within 2.2e-16 of
+// glibc's. The bounds kApxRadRel / kApxAng are verified over EVERY MRG32k3a
+// uniform against the glibc-exact qt_math.h (k_apx_bounds_check,
+// tests/test_fast_path.py). Build with -DQT_APX_FULL for the previous ~1 ulp
+// evaluation (hi + lo sums, degree-8 tail, three-part reduction): 4.5 % slower
+// at C2 (1.325e11 vs 1.389e11 transitions/s) for no change in the counts.
 #pragma once
 
 #include <stdint.h>
@@ -158,13 +162,14 @@ static __device__ const LogEntry kLogTab[128] = {
 // constants (constant bank: DFMA takes them as c[][] operands)
 struct Consts {
   double ln2_hi, ln2_lo;          // ln 2 with a 41-bit head (k ln2_hi exact)
+  double ln2;                     // ln 2 rounded to double
   double l2, l3, l4, l5, l6, l7, l8;  // log1p tail: 1/3, -1/4, 1/5, -1/6, 1/7, -1/8 (+ -1/2)
   double s1, s2, s3, s4, s5, s6;  // fdlibm __kernel_sin
   double c1, c2, c3, c4, c5, c6;  // fdlibm __kernel_cos
   double two_over_pi, pio2_hi, pio2_mid, pio2_lo;
 };
 static __constant__ Consts kC = {
-    0x1.62e42fefa4000p-1, -0x1.8432a1b0e2634p-43,
+    0x1.62e42fefa4000p-1, -0x1.8432a1b0e2634p-43, 0x1.62e42fefa39efp-1,
     -0.5, 0x1.5555555555555p-2, -0.25, 0x1.999999999999ap-3, -0x1.5555555555555p-3,
     0x1.2492492492492p-3, -0.125,
     -1.66666666666666324348e-01, 8.33333333332248946124e-03, -1.98412698298579493134e-04,
@@ -176,6 +181,53 @@ static __constant__ Consts kC = {
 // log(u), u a positive normal <= 1: u = 2^e m, m in [1, 2); cell i = round(128 (m - 1))
 // (the top cell folds to m/2 next to 1); r = m invc_i - 1 by one FMA, |r| <= 2^-8;
 // log u = e ln2 + (-log invc_i) + log1p(r) with hi + lo sums and a degree-8 tail.
+#if !defined(QT_APX_FULL)
+// The certified kernel's log: the same table and reduction, the result as one FMA
+// and two additions (no hi + lo compensation) and a degree-6 tail. ~1e-15 relative
+// instead of ~1 ulp; the bound below is what k_apx_bounds_check verifies.
+__device__ __forceinline__ double log_unit(double u) {
+  const long long b = __double_as_longlong(u);
+  int e = static_cast<int>(b >> 52) - 1023;
+  const long long mant = b & ((1ll << 52) - 1);
+  int i = static_cast<int>((mant + (1ll << 44)) >> 45);
+  double m = __longlong_as_double(mant | (1023ll << 52));
+  if (i == 128) {
+    i = 0;
+    e += 1;
+    m = __dmul_rn(m, 0.5);
+  }
+  const double2 t = __ldg(reinterpret_cast<const double2*>(&kLogTab[i]));
+  const double r = __fma_rn(m, t.x, -1.0);
+  double p = __fma_rn(r, kC.l6, kC.l5);
+  p = __fma_rn(r, p, kC.l4);
+  p = __fma_rn(r, p, kC.l3);
+  p = __fma_rn(r, p, kC.l2);
+  const double hi = __fma_rn(static_cast<double>(e), kC.ln2, t.y);
+  return __dadd_rn(hi, __fma_rn(__dmul_rn(r, r), p, r));
+}
+
+// sin and cos of a in [0, 2 pi]: Cody-Waite by q pi/2 in two parts (the third
+// part and the reduction tail dropped), the fdlibm polynomials without their
+// tail corrections.
+__device__ __forceinline__ void sincos(double a, double* s_out, double* c_out) {
+  const double q = rint(__dmul_rn(a, kC.two_over_pi));
+  const double r = __fma_rn(-q, kC.pio2_mid, __fma_rn(-q, kC.pio2_hi, a));
+  const double z = __dmul_rn(r, r);
+  const double ps =
+      __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, kC.s6, kC.s5), kC.s4), kC.s3), kC.s2),
+               kC.s1);
+  const double sn = __fma_rn(__dmul_rn(z, r), ps, r);
+  const double pc =
+      __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, kC.c6, kC.c5), kC.c4), kC.c3), kC.c2),
+               kC.c1);
+  const double cs = __fma_rn(__dmul_rn(z, z), pc, __fma_rn(-0.5, z, 1.0));
+  const int quad = static_cast<int>(q) & 3;
+  const double s1 = (quad & 1) ? cs : sn;
+  const double c1 = (quad & 1) ? sn : cs;
+  *s_out = (quad & 2) ? -s1 : s1;
+  *c_out = ((quad + 1) & 2) ? -c1 : c1;
+}
+#else
 __device__ __forceinline__ double log_unit(double u) {
   const long long b = __double_as_longlong(u);
   int e = static_cast<int>(b >> 52) - 1023;
@@ -232,6 +284,7 @@ __device__ __forceinline__ void sincos(double a, double* s_out, double* c_out) {
   *s_out = (quad & 2) ? -s1 : s1;
   *c_out = ((quad + 1) & 2) ? -c1 : c1;
 }
+#endif
 
 // The Box-Muller radius sqrt(-2 log u1) of the certified kernel.
 // (The correctly rounded __dsqrt_rn measured faster than an rsqrt seed plus
@@ -241,12 +294,20 @@ __device__ __forceinline__ double radius(double u) { return __dsqrt_rn(__dmul_rn
 // Verified bounds against the glibc-exact pair (k_apx_bounds_check, every MRG32k3a
 // output as u1 and as u2): |r~ - r| <= kApxRadRel r with r = sqrt(-2 log u1), and
 // |c~ - c|, |s~ - s| <= kApxAng with (c, s) = (cos, sin)(2 pi u2); |c~|, |s~| <= 1.
-// Measured on B200 (qt_apx_bounds_check): 2.2e-16 and 1.1e-16; the constants keep 2x.
-constexpr double kApxRadRel = 0x1p-51;  // 4.4e-16
-constexpr double kApxAng = 0x1p-52;     // 2.2e-16
+#if !defined(QT_APX_FULL)
+// Measured on B200 (qt_apx_bounds_check): 8.43e-15 (0x1.2fdap-47) and 2.2e-16
+// (2^-52); the constants keep >= 2x.
+constexpr double kApxRadRel = 0x1p-45;  // 2.8e-14
+constexpr double kApxAng = 0x1p-51;     // 4.4e-16
 // |z~ - z| <= r~ kApxZ for z = RN(r c) (and the mate RN(r s)): |r~c~ - rc| <=
 // r (kApxRadRel + kApxAng), two product roundings 2^-53 r each, r <= r~ / (1 - kApxRadRel)
+constexpr double kApxZ = 0x1.1p-45;     // >= (2^-45 + 2^-51 + 2^-52) (1 + 2^-40) = 0x1.06p-45 (1 + 2^-40)
+#else
+// Measured on B200: 2.2e-16 and 1.1e-16; the constants keep 2x.
+constexpr double kApxRadRel = 0x1p-51;  // 4.4e-16
+constexpr double kApxAng = 0x1p-52;     // 2.2e-16
 constexpr double kApxZ = 0x1.2p-50;     // >= (2^-51 + 2^-52 + 2^-52) (1 + 2^-40) = 2^-50 (1 + 2^-40)
+#endif
 
 }  // namespace apx
 }  // namespace qt
