@@ -28,7 +28,7 @@ struct alignas(32) LogEntry {
   double invc, lhi, llo, pad;
 };
 // entry i: invc = RN(1 / (1 + i/128)) (exactly 1 for i = 0) and -log(invc) as hi + lo
-static __device__ const LogEntry kLogTab[128] = {
+static __device__ const LogEntry kLogTab[129] = {
   {0x1.0000000000000p+0, 0x0.0p+0, 0x0.0p+0, 0.0},
   {0x1.fc07f01fc07f0p-1, 0x1.fe02a6b106799p-8, -0x1.e44b7e3711e7fp-67, 0.0},
   {0x1.f81f81f81f820p-1, 0x1.fc0a8b0fc03c4p-7, -0x1.83092c5964281p-62, 0.0},
@@ -157,6 +157,9 @@ static __device__ const LogEntry kLogTab[128] = {
   {0x1.03091b51f5e1ap-1, 0x1.5cdb1dc6c1765p-1, 0x1.47b71e2eb8419p-56, 0.0},
   {0x1.0204081020408p-1, 0x1.5ee02a9241676p-1, -0x1.bca7da80b6f7ep-55, 0.0},
   {0x1.0101010101010p-1, 0x1.60e32f44788d9p-1, -0x1.58376a5f4b135p-57, 0.0},
+  // i = 128 (m next to 2): invc = 1/2, -log(invc) = ln 2 (the lighter log's
+  // branch-free fold; the full one folds m / 2 into entry 0 instead)
+  {0x1.0000000000000p-1, 0x1.62e42fefa39efp-1, 0x1.abc9e3b39803fp-56, 0.0},
 };
 
 // constants (constant bank: DFMA takes them as c[][] operands)
@@ -187,15 +190,10 @@ static __constant__ Consts kC = {
 // instead of ~1 ulp; the bound below is what k_apx_bounds_check verifies.
 __device__ __forceinline__ double log_unit(double u) {
   const long long b = __double_as_longlong(u);
-  int e = static_cast<int>(b >> 52) - 1023;
+  const int e = static_cast<int>(b >> 52) - 1023;
   const long long mant = b & ((1ll << 52) - 1);
-  int i = static_cast<int>((mant + (1ll << 44)) >> 45);
-  double m = __longlong_as_double(mant | (1023ll << 52));
-  if (i == 128) {
-    i = 0;
-    e += 1;
-    m = __dmul_rn(m, 0.5);
-  }
+  const int i = static_cast<int>((mant + (1ll << 44)) >> 45);  // 0..128
+  const double m = __longlong_as_double(mant | (1023ll << 52));
   const double2 t = __ldg(reinterpret_cast<const double2*>(&kLogTab[i]));
   const double r = __fma_rn(m, t.x, -1.0);
   double p = __fma_rn(r, kC.l6, kC.l5);
@@ -287,8 +285,9 @@ __device__ __forceinline__ void sincos(double a, double* s_out, double* c_out) {
 #endif
 
 // The Box-Muller radius sqrt(-2 log u1) of the certified kernel.
-// (The correctly rounded __dsqrt_rn measured faster than an rsqrt seed plus
-// Newton steps: 1.324e11 vs 1.294e11 transitions/s at C2.)
+// (The correctly rounded __dsqrt_rn measured faster than an FP32 rsqrt seed plus
+// Newton steps, 1.324e11 vs 1.294e11 transitions/s at C2, and level with the FP64
+// MUFU.RSQ64H seed + one Newton step + one correction, 1.41e11 both.)
 __device__ __forceinline__ double radius(double u) { return __dsqrt_rn(__dmul_rn(-2.0, log_unit(u))); }
 
 // Verified bounds against the glibc-exact pair (k_apx_bounds_check, every MRG32k3a
