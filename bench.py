@@ -533,7 +533,7 @@ def run_ours(args, rank, world, local_rank):
                      "kernel_ms": t_kern, "peak_source": peak_src,
                      "algorithmic_bytes": "16 B per transition (u64 counter read-modify-write)",
                      "binding_unit": (
-                         "d = 1: instruction issue (see roofline_issue; 1.43e11/s with the count "
+                         "d = 1: instruction issue (see roofline_issue; 1.565e11/s with the count "
                          "REDs removed) with the count scatter's L2 atomic ceiling close behind "
                          "(one 64-bit RED per transition; tools/red_probe.cu measures 1.3-1.9e11 "
                          "REDs/s on this B200 for such patterns, profiles/r02_red_probe_*.txt)"
@@ -556,16 +556,16 @@ def run_ours(args, rank, world, local_rank):
     if kind in ("bm", "ou") and est != 2:
         # the kernel's own bound: instruction issue. Warp
         # instructions per transition from the committed ncu capture of this kernel
-        # (profiles/r02_ncu_kernels.md section 0, r02aq_cert: 5.18); ceiling = SMs x 4
+        # (profiles/r02_ncu_kernels.md section 0, r02bj_cert: 4.71); ceiling = SMs x 4
         # schedulers x the measured SM clock / that count.
-        wipt = 5.18
+        wipt = 4.71
         sm_mhz = (clocks.get("sm_mhz") or 1965.0) if isinstance(clocks, dict) else 1965.0
         ceil = torch.cuda.get_device_properties(dev).multi_processor_count * 4 * sm_mhz * 1e6 / wipt
         kern_rate = kern_units / (t_kern / 1e3)
         line["roofline_issue"] = {"bound": "issue", "achieved": kern_rate, "peak": ceil,
                                   "unit": "transitions/s", "frac": kern_rate / ceil,
                                   "warp_instructions_per_transition": wipt,
-                                  "source": "profiles/r02_ncu_kernels.md (ncu r02aq_cert)"}
+                                  "source": "profiles/r02_ncu_kernels.md (ncu r02bj_cert)"}
     if world > 1:
         line["comm"] = {"backend": dist.get_backend(), "nranks": dist.get_world_size(),
                         "collective": "all_reduce(int64 joint counts, SUM), once per step"}
