@@ -1273,7 +1273,16 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
         xa.ojoint = reinterpret_cast<unsigned long long*>(d_joint);
         mrg_back_jump(2 * ((static_cast<uint64_t>(p->n) + 1) / 2), xa.back);
       }
-      const size_t xsmem = resident ? p->total_tab : static_cast<size_t>(xa.stages) * buf;
+      size_t xsmem = resident ? p->total_tab : static_cast<size_t>(xa.stages) * buf;
+      // the first transition's single row (x0 -> N_1 cells: every path hits it) is
+      // counted per CTA in shared memory: at C1 the row takes 1e6 REDs on 7 L2 lines
+      xa.n1 = 0;
+      const char* h1 = std::getenv("QT_X_HIST1");
+      if (!(h1 && h1[0] == '0') && p->sizes[1] <= 16384) {
+        xa.hist1_off = static_cast<uint32_t>((xsmem + 15) & ~size_t(15));
+        xa.n1 = static_cast<uint32_t>(p->sizes[1]);
+        xsmem = xa.hist1_off + 4ull * xa.n1;
+      }
       int xbps = 1;
       QT_CUDA(qt::launch_paths_x(p->kind, resident, P, cert, xa, 0, xsmem, st, &xbps));
       uint64_t xblocks = static_cast<uint64_t>(p->sm_count) * xbps;
@@ -1283,6 +1292,7 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       const uint64_t T = xblocks * per_block;
       xa.q = count / T;
       xa.rem = count % T;
+      if ((xa.q + 1) * per_block >= (1ull << 31)) xa.n1 = 0;  // u32 per-CTA counters
       xa.joint = p->d_sjoint;
       xa.xtables = p->d_xtables;
       QT_CUDA(qt::launch_paths_x(p->kind, resident, P, cert, xa, static_cast<uint32_t>(xblocks),

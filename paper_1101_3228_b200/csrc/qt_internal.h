@@ -83,6 +83,12 @@ struct PathArgs {
   uint64_t amb_cap;
   unsigned long long* ojoint;
   uint32_t back[18];          // (J^D)^-1: path end state -> path start state
+  // k_paths_x: the first transition (x0 -> layer 1: every path lands in one of
+  // N_1 cells of a single row) counted in a per-CTA shared-memory histogram of
+  // n1 u32 at byte offset hist1_off of the dynamic smem, flushed once per CTA;
+  // n1 = 0: one RED per path like the other layers
+  uint32_t n1;
+  uint32_t hist1_off;
 };
 
 constexpr int kPathConsumers = 256;  // consumer threads per k_paths CTA

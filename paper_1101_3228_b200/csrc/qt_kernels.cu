@@ -464,7 +464,7 @@ template <int K, int P, bool CERT>
 __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act)[P],
                                             const uint8_t* tb, uint32_t k,
                                             unsigned long long* joint, const uint8_t* gtables,
-                                            bool count) {
+                                            bool count, uint32_t* hist1) {
   using C = Chain<K>;
   const LayerTable& h = *reinterpret_cast<const LayerTable*>(tb);
   const double x_safe = h.x_safe, lo = h.lo, inv_w = h.inv_w, nb_d = h.nb_d;
@@ -546,7 +546,8 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
       j = in0 ? c[p] : c[p] + 1;
       if (act[p] && ps[p].amb_k == 0) {
         if (safe[p] && (in0 || in1)) {
-          if (count) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + j, 1ull);
+          if (hist1 && k == 1) atomicAdd(hist1 + j, 1u);  // row 0 of joint[0], per CTA
+          else if (count) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + j, 1ull);
         } else {
           ps[p].amb_k = k;
         }
@@ -566,7 +567,10 @@ __device__ __forceinline__ void exact_layer(ExactPath (&ps)[P], const bool (&act
       } else {  // exact scan over the cold block (NaN / inf / |x| >= x_safe)
         j = nearest_1d_scan_pos(reinterpret_cast<const Rec1*>(gtables + h.cold_off), npts, x);
       }
-      if (act[p] && count) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + j, 1ull);
+      if (act[p]) {
+        if (hist1 && k == 1) atomicAdd(hist1 + j, 1u);
+        else if (count) red_add_u64(jl + static_cast<uint64_t>(ps[p].i) * npts + j, 1ull);
+      }
     }
     ps[p].i = j;
   }
@@ -582,6 +586,8 @@ __global__ void __launch_bounds__(kXThreads, QT_X_MINB) k_paths_x(const __grid_c
   const uint32_t tid = threadIdx.x;
   const uint32_t S = a.stages;
   const uint32_t spr = (a.n + L - 1) / L;  // stage steps per round
+  uint32_t* hist1 = a.n1 ? reinterpret_cast<uint32_t*>(smem + a.hist1_off) : nullptr;
+  for (uint32_t c = tid; c < a.n1; c += kXThreads) hist1[c] = 0u;
   const uint64_t rounds = a.q + (a.rem ? 1u : 0u);
   const uint64_t steps_total = rounds * spr;
   if (steps_total == 0) return;
@@ -644,10 +650,10 @@ __global__ void __launch_bounds__(kXThreads, QT_X_MINB) k_paths_x(const __grid_c
       } else {
         mbar_wait_u32(full0 + 8u * s, ph);
       }
-      exact_layer<K, P, CERT>(ps, act, tb, k, a.joint, a.tables, a.probe_nored == 0);
+      exact_layer<K, P, CERT>(ps, act, tb, k, a.joint, a.tables, a.probe_nored == 0, hist1);
       if (L == 2 && k + 1 <= a.n)  // the next table follows this one (header.bytes)
         exact_layer<K, P, CERT>(ps, act, tb + reinterpret_cast<const LayerTable*>(tb)->bytes,
-                                k + 1, a.joint, a.tables, a.probe_nored == 0);
+                                k + 1, a.joint, a.tables, a.probe_nored == 0, hist1);
       if constexpr (!RESIDENT) {
         named_barrier_sync(1, kXThreads);  // every thread is done with stage s
         if (tid == 0 && g + S < steps_total) issue(g + S);
@@ -685,6 +691,11 @@ __global__ void __launch_bounds__(kXThreads, QT_X_MINB) k_paths_x(const __grid_c
         }
       }
     }
+  }
+  if (hist1) {  // the CTA's first-transition counts: one RED per visited cell of row 0
+    __syncthreads();
+    for (uint32_t c = tid; c < a.n1; c += kXThreads)
+      if (hist1[c]) red_add_u64(a.joint + c, static_cast<unsigned long long>(hist1[c]));
   }
 }
 

@@ -278,3 +278,28 @@ def test_alg3_count_tile_equals_l2_reds(gpu, monkeypatch, mode):
     reds = _counts3(plan, M, n, mode)
     assert tile.sum() == M * n
     assert np.array_equal(tile, reds)
+
+
+@pytest.mark.parametrize("mode", [2, 0])
+def test_first_transition_histogram_equals_reds(gpu, monkeypatch, mode):
+    """k_paths_x counts the first transition (x0 -> layer 1, a single row every
+    path hits) in a per-CTA shared-memory histogram; QT_X_HIST1=0 issues one RED
+    per path instead. Same counts, certified (mode 2) and exact (mode 0)."""
+    import torch
+    from paper_1101_3228_b200.device import Plan
+    q = Q()
+    ch = q.BrownianChain1d(10)
+    plan = Plan(ch, q.build_brownian_grids(ch, 100), 0)
+    q.set_fast_path(mode)
+    try:
+        out = []
+        for h in ("1", "0"):
+            monkeypatch.setenv("QT_X_HIST1", h)
+            joint = plan.zeros_joint()
+            plan.count(1, 1, 12345, 777, 300001, 10**6, joint)
+            torch.cuda.synchronize()
+            out.append(joint.cpu().numpy().view(np.uint64).copy())
+    finally:
+        q.set_fast_path(True)
+    assert out[0][:100].sum() == 300001
+    assert np.array_equal(out[0], out[1])
