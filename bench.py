@@ -374,7 +374,7 @@ def run_ours(args, rank, world, local_rank):
             # repeated within a step (same units, counts accumulate, value
             # counts every pass) so the timed region carries clock evidence;
             # calibrated on a warm step, the last warm-up step runs with it
-            t1 = torch.tensor([ev[0].elapsed_time(ev[3])], dtype=torch.float64, device=dev)
+            t1 = torch.tensor([ev[1].elapsed_time(ev[2])], dtype=torch.float64, device=dev)  # one pass
             if world > 1:
                 dist.all_reduce(t1, op=dist.ReduceOp.MAX)
             reps = max(1, math.ceil(args.min_step_ms / max(float(t1[0]), 1e-3)))
