@@ -211,6 +211,30 @@ def test_one_call_plan_cache_is_keyed_by_inputs(gpu, oracle):
         assert np.array_equal(t.flat_visits, ref.visits)
 
 
+def test_plan_cache_clear_and_disable(gpu, monkeypatch):
+    """qt_plan_cache_clear() drops the cached plans (their device memory is
+    freed: the next call rebuilds), QT_PLAN_CACHE=0 keeps none; results equal
+    the cached call's either way."""
+    import torch
+    q = Q()
+    ch = q.BrownianChain1d(10)
+    grids = q.build_brownian_grids(ch, 100)
+    a = q.estimate_alg2(ch, grids, 200000)
+    torch.cuda.synchronize()
+    q.plan_cache_clear()
+    free0 = torch.cuda.mem_get_info()[0]
+    b = q.estimate_alg2(ch, grids, 200000)  # rebuilt and cached again
+    torch.cuda.synchronize()
+    assert torch.cuda.mem_get_info()[0] < free0  # the new plan holds device memory
+    q.plan_cache_clear()
+    assert torch.cuda.mem_get_info()[0] >= free0  # and clearing returns it
+    monkeypatch.setenv("QT_PLAN_CACHE", "0")
+    c = q.estimate_alg2(ch, grids, 200000)
+    for t in (b, c):
+        assert np.array_equal(t.flat_joint, a.flat_joint)
+        assert np.array_equal(t.flat_pi, a.flat_pi)
+
+
 def test_c1_config_bit_exact(gpu, oracle, golden):
     """BASELINE config 1: 1-D BS put, n=10, N=100, M=1e6, MRG32k3a seed 12345."""
     q = Q()
