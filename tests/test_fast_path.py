@@ -303,3 +303,25 @@ def test_first_transition_histogram_equals_reds(gpu, monkeypatch, mode):
         q.set_fast_path(True)
     assert out[0][:100].sum() == 300001
     assert np.array_equal(out[0], out[1])
+
+
+def test_alg3_count_tile_ragged_layers(gpu, monkeypatch):
+    """The Alg III count tile with layer sizes that differ from layer to layer
+    (the tile is sized for the largest N_{k-1} x N_k, each layer uses its own
+    N_{k-1} x N_k block) equals the one-RED-per-sample kernel."""
+    from paper_1101_3228_b200.device import Plan
+    q = Q()
+    n = 9
+    ch = q.OuChain1d(q.TwoFactorParams(sigma1=0.5, alpha1=1.0, sigma2=0.0, steps=n))
+    rng = np.random.default_rng(21)
+    sizes = [37, 250, 3, 120, 199, 64, 1, 90, 180]
+    grids = [q.QuantGrid(1, np.sort(rng.standard_normal(s)) * 0.5 + 0.01 * k)
+             for k, s in enumerate(sizes)]
+    plan = Plan(ch, grids, 0)
+    M = 120001
+    monkeypatch.setenv("QT_A3_SLICES", "2")
+    tile = _counts3(plan, M, n, 2)
+    monkeypatch.setenv("QT_A3_PRIV", "0")
+    reds = _counts3(plan, M, n, 2)
+    assert tile.sum() == M * n
+    assert np.array_equal(tile, reds)
