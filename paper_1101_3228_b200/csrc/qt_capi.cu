@@ -135,19 +135,29 @@ Mat3 mat_mul(const Mat3& x, const Mat3& y, uint64_t m) {
   return r;
 }
 
-// J^(2^b), b = 0..63, both components: [b][0..8] = m1 part, [b][9..17] = m2 part
+// J^(d 16^w), w = 0..15 (4-bit windows of the jump), d = 1..15, both components:
+// entry 15 w + d - 1 = [0..8] the m1 part, [9..17] the m2 part. A jump by e applies
+// one entry per non-zero hex digit of e (at most 16 instead of 64 squarings' worth).
 std::vector<uint32_t> mrg_jump_table() {
-  Mat3 c1{{{0, 1, 0}, {0, 0, 1}, {kM1 - 810728ull, 1403580ull, 0}}};
-  Mat3 c2{{{0, 1, 0}, {0, 0, 1}, {kM2 - 1370589ull, 0, 527612ull}}};
-  std::vector<uint32_t> t(64 * 18);
-  for (int b = 0; b < 64; ++b) {
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) {
-        t[b * 18 + 3 * i + j] = static_cast<uint32_t>(c1.a[i][j]);
-        t[b * 18 + 9 + 3 * i + j] = static_cast<uint32_t>(c2.a[i][j]);
-      }
-    c1 = mat_mul(c1, c1, kM1);
-    c2 = mat_mul(c2, c2, kM2);
+  Mat3 p1{{{0, 1, 0}, {0, 0, 1}, {kM1 - 810728ull, 1403580ull, 0}}};  // J^(16^w)
+  Mat3 p2{{{0, 1, 0}, {0, 0, 1}, {kM2 - 1370589ull, 0, 527612ull}}};
+  std::vector<uint32_t> t(16 * 15 * 18);
+  for (int w = 0; w < 16; ++w) {
+    Mat3 c1 = p1, c2 = p2;  // J^(d 16^w)
+    for (int d = 1; d <= 15; ++d) {
+      const int b = 15 * w + d - 1;
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+          t[b * 18 + 3 * i + j] = static_cast<uint32_t>(c1.a[i][j]);
+          t[b * 18 + 9 + 3 * i + j] = static_cast<uint32_t>(c2.a[i][j]);
+        }
+      c1 = mat_mul(c1, p1, kM1);
+      c2 = mat_mul(c2, p2, kM2);
+    }
+    for (int q = 0; q < 4; ++q) {  // p <- p^16
+      p1 = mat_mul(p1, p1, kM1);
+      p2 = mat_mul(p2, p2, kM2);
+    }
   }
   return t;
 }
@@ -191,11 +201,12 @@ Mat3 mat_pow_inv(Mat3 c, uint64_t e, uint64_t m) {
 // s[0..2] component 1, s[3..5] component 2, oldest first.
 void mrg_skip_host(uint64_t s[6], uint64_t e) {
   static const std::vector<uint32_t> J = mrg_jump_table();
-  for (int b = 0; e != 0; ++b, e >>= 1) {
-    if (!(e & 1ull)) continue;
+  for (int w = 0; e != 0; ++w, e >>= 4) {
+    const int d = static_cast<int>(e & 15u);
+    if (!d) continue;
     for (int c = 0; c < 2; ++c) {
       const uint64_t m = c ? kM2 : kM1;
-      const uint32_t* M = J.data() + b * 18 + 9 * c;
+      const uint32_t* M = J.data() + (15 * w + d - 1) * 18 + 9 * c;
       uint64_t r[3];
       for (int i = 0; i < 3; ++i) {
         u128 acc = 0;

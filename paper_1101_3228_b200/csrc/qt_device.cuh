@@ -144,12 +144,15 @@ __device__ __forceinline__ void mat_apply_m2(const uint32_t* J, uint32_t& x0, ui
   x2 = r[2];
 }
 
-// state <- J^e state (mrg32k3a_skip, mrg32k3a.hpp:124-146), O(log e)
+// state <- J^e state (mrg32k3a_skip, mrg32k3a.hpp:124-146): one table entry
+// J^(d 16^w) per non-zero hex digit d of e (the table is mrg_jump_table, qt_capi.cu)
 __device__ __forceinline__ void mrg_jump(Mrg& s, uint64_t e, const uint32_t* table) {
-  for (int b = 0; e != 0; ++b, e >>= 1) {
-    if (e & 1ull) {
-      mat_apply_m1(table + b * 18, s.a0, s.a1, s.a2);
-      mat_apply_m2(table + b * 18 + 9, s.b0, s.b1, s.b2);
+  for (int w = 0; e != 0; ++w, e >>= 4) {
+    const uint32_t d = static_cast<uint32_t>(e & 15u);
+    if (d) {
+      const uint32_t* J = table + (15u * w + d - 1u) * 18u;
+      mat_apply_m1(J, s.a0, s.a1, s.a2);
+      mat_apply_m2(J + 9, s.b0, s.b1, s.b2);
     }
   }
 }
