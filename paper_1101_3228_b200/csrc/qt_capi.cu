@@ -1242,7 +1242,9 @@ int plan_count(qt_plan* p, int alg, int engine, uint64_t seed, uint64_t first, u
       // d_joint (calls on one plan are ordered by their streams: one scratch)
       if (!p->d_sjoint) QT_CUDA(cudaMalloc(&p->d_sjoint, p->njoint * sizeof(uint64_t)));
       QT_CUDA(cudaMemsetAsync(p->d_sjoint, 0, p->njoint * sizeof(uint64_t), st));
-      int P = 2;
+      // paths in flight per thread: 2 (C2 1.33e11 vs 1.06e11 with 1); 1 when every
+      // thread slot would run only a few paths (C1, 7 rounds: 1.05e11 vs 9.9e10 with 2)
+      int P = count < static_cast<uint64_t>(p->sm_count) * 2 * qt::kXThreads * 2 * 64 ? 1 : 2;
       if (const char* e = std::getenv("QT_X_P")) P = std::atoi(e) == 1 ? 1 : std::atoi(e) == 4 ? 4 : 2;
       qt::PathArgs xa = a;
       // layers per pipeline stage (1 or 2)

@@ -325,3 +325,24 @@ def test_alg3_count_tile_ragged_layers(gpu, monkeypatch):
     reds = _counts3(plan, M, n, 2)
     assert tile.sum() == M * n
     assert np.array_equal(tile, reds)
+
+
+@pytest.mark.parametrize("mode", [2, 0])
+def test_paths_per_thread_variants_agree(gpu, monkeypatch, mode):
+    """k_paths_x runs one path per thread for small path counts and two for
+    large ones (a heuristic on the count); both variants, forced through
+    QT_X_P, give the same counts on the same window."""
+    from paper_1101_3228_b200.device import Plan
+    q = Q()
+    ch = q.BrownianChain1d(50)
+    plan = Plan(ch, q.build_brownian_grids(ch, 500), 0)
+    q.set_fast_path(mode)
+    try:
+        out = []
+        for pp in ("1", "2"):
+            monkeypatch.setenv("QT_X_P", pp)
+            out.append(_counts(plan, 400003, 123456789, 10**9, fast=mode))
+    finally:
+        q.set_fast_path(True)
+    assert out[0][:500].sum() == 400003
+    assert np.array_equal(out[0], out[1])
