@@ -157,6 +157,9 @@ class ClockSampler:
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        t0 = time.perf_counter()  # nvidia-smi takes a while to start: sample from the first step
+        while not self.lines and time.perf_counter() - t0 < 3.0:
+            time.sleep(0.01)
 
     def _read(self):
         for line in self.proc.stdout:
